@@ -1,0 +1,242 @@
+"""Generate golden vectors by running the REAL reference implementation.
+
+Run in the build container only (it imports `voxsplat` from the read-only
+reference tree):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Outputs small `.npz` fixtures next to this script.  They hold the inputs
+and the reference's outputs, so the GPU box (which has no /root/reference)
+can check both the oracle and the CUDA path against them.
+
+Fixtures
+  gpr_problems.npz   random problems of the reference tests (seeds 7, 101,
+                     tests/_oracles.py:80-89) + closed form + interpolation;
+                     outputs of voxsplat.gpr.gpr_solve (gpr.py:173-205)
+  keys.npz           voxel_keys (voxel_map.py:136-143) incl. boundary values
+  axis.npz           select_value_axis (gpr.py:57-78) on planar/degenerate sets
+  grids.npz          make_mesh_grid (gpr.py:104-120) for several (n_s, n_r)
+  subgrids.npz       init_position / init_covariance (splat_init.py:92-114)
+  scan_frames.npz    3-frame mapping replay through MappingPipeline.ingest_frame
+                     (pipeline.py:139-187): update order, per-voxel counts,
+                     transitions, predictions, Gaussian map
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+REF_TESTS = "/root/reference/pkg/tests"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, REF_TESTS)
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+
+from voxsplat import Camera, PipelineConfig  # noqa: E402
+from voxsplat import gpr as rgpr  # noqa: E402
+from voxsplat import splat_init as rsplat  # noqa: E402
+from voxsplat import voxel_map as rvm  # noqa: E402
+from voxsplat.errors import DegenerateGeometryError  # noqa: E402
+from voxsplat.pipeline import FrameSample, MappingPipeline  # noqa: E402
+from _oracles import random_gpr_problem  # noqa: E402
+
+from workloads import scenes  # noqa: E402
+
+
+def pack_problems(problems):
+    n = np.array([len(p[0]) for p in problems], dtype=np.int64)
+    m = np.array([len(p[3]) for p in problems], dtype=np.int64)
+    return dict(
+        n=n, m=m, lam=np.array([p[4] for p in problems]),
+        x=np.concatenate([p[0] for p in problems]),
+        f=np.concatenate([p[1] for p in problems]),
+        noise=np.concatenate([p[2] for p in problems]),
+        xs=np.concatenate([p[3] for p in problems]))
+
+
+def gpr_fixture():
+    out = {}
+    for seed, count, nmax in ((7, 100, 64), (101, 100, 64), (11, 200, 24)):
+        rng = np.random.default_rng(seed)
+        probs = [random_gpr_problem(rng, n_max=nmax, m_max=81 if nmax > 24 else 36)
+                 for _ in range(count)]
+        pk = pack_problems(probs)
+        mus, vs, fulls = [], [], []
+        for i, (x, f, noise, xs, lam) in enumerate(probs):
+            r = rgpr.gpr_solve(rgpr.GprProblem(x, f, noise, xs, lam),
+                               return_full=(seed == 7 and i < 8))
+            mus.append(r.mu_star)
+            vs.append(r.sigma_star_diag)
+            if r.sigma_star_full is not None:
+                fulls.append(r.sigma_star_full.ravel())
+        pk["mu"] = np.concatenate(mus)
+        pk["var"] = np.concatenate(vs)
+        if fulls:
+            pk["full"] = np.concatenate(fulls)
+        for k, v in pk.items():
+            out[f"s{seed}_{k}"] = v
+    # closed form (tests/test_gpr.py:143-147)
+    r = rgpr.gpr_solve(rgpr.GprProblem(x=[[0, 0]], f=[2.0], noise_diag=[0.25],
+                                       x_star=[[0, 0]]))
+    out["closed_mu"], out["closed_var"] = r.mu_star, r.sigma_star_diag
+    # noiseless interpolation (tests/test_gpr.py:149-162)
+    rng = np.random.default_rng(6)
+    gx, gy = np.meshgrid(np.linspace(0, 1, 5), np.linspace(0, 1, 5))
+    x = np.column_stack([gx.ravel(), gy.ravel()]) + rng.uniform(-0.05, 0.05, (25, 2))
+    f = np.sin(3 * x[:, 0]) + x[:, 1]
+    r = rgpr.gpr_solve(rgpr.GprProblem(x=x, f=f, noise_diag=np.zeros(25),
+                                       x_star=x, lam=25.0))
+    out.update(interp_x=x, interp_f=f, interp_mu=r.mu_star, interp_var=r.sigma_star_diag)
+    np.savez_compressed(os.path.join(HERE, "gpr_problems.npz"), **out)
+
+
+def keys_fixture():
+    rng = np.random.default_rng(20)
+    pts = rng.uniform(-3, 3, (2000, 3))
+    # exact lattice boundaries and near-boundary values
+    grid = np.arange(-10, 11) * 0.2
+    edge = np.stack([grid, grid[::-1], np.roll(grid, 3)], axis=1)
+    nudged = np.concatenate([edge, np.nextafter(edge, -np.inf), np.nextafter(edge, np.inf)])
+    pts = np.concatenate([pts, nudged, [[0.05, 0.19, -0.01], [0.0, 0.0, 0.0]]])
+    np.savez_compressed(os.path.join(HERE, "keys.npz"), points=pts,
+                        keys_02=rvm.voxel_keys(pts, 0.2), keys_05=rvm.voxel_keys(pts, 0.5))
+
+
+def axis_fixture():
+    rng = np.random.default_rng(21)
+    sets, axes = [], []
+    for i in range(300):
+        n = int(rng.integers(3, 120))
+        normal = rng.normal(size=3)
+        normal /= np.linalg.norm(normal)
+        basis = np.linalg.svd(normal[None, :])[2][1:]
+        pts = rng.uniform(-0.25, 0.25, (n, 2)) @ basis
+        pts += rng.uniform(0.0, 0.03) * rng.normal(size=(n, 1)) * normal
+        pts += rng.uniform(-5, 5, 3)
+        if i % 25 == 0:
+            pts = np.full((n, 3), 0.3)            # coincident
+        elif i % 25 == 1:
+            pts = np.outer(np.linspace(0, 1, n), rng.normal(size=3))  # collinear
+        sets.append(pts)
+        try:
+            axes.append(rgpr.select_value_axis(pts).value_axis)
+        except DegenerateGeometryError:
+            axes.append(-1)
+    np.savez_compressed(os.path.join(HERE, "axis.npz"),
+                        n=np.array([len(s) for s in sets]),
+                        points=np.concatenate(sets), axis=np.array(axes))
+
+
+def grids_fixture():
+    out = {}
+    cases = [((0.0, 0.2), (0.0, 0.2), 3, 3), ((0.4, 0.6), (-1.2, -1.0), 1, 1),
+             ((-3.5, -3.0), (12.0, 12.5), 2, 2), ((0.0, 0.9), (0.0, 0.9), 4, 3),
+             ((1.3, 1.8), (-0.5, 0.0), 4, 4), ((7.1, 7.3), (2.2, 2.4), 3, 2)]
+    for i, (e0, e1, ns, nr) in enumerate(cases):
+        out[f"g{i}_extent"] = np.array([e0, e1], dtype=np.float64)
+        out[f"g{i}_nsnr"] = np.array([ns, nr])
+        out[f"g{i}_grid"] = rgpr.make_mesh_grid((e0, e1), ns, nr)
+    np.savez_compressed(os.path.join(HERE, "grids.npz"), **out)
+
+
+def subgrid_fixture():
+    rng = np.random.default_rng(106)
+    pts = rng.uniform(-1, 1, (200, 9, 3))
+    w = rng.uniform(0.05, 20.0, (200, 9))
+    pos, phi, scale = [], [], []
+    for i in range(200):
+        g = rsplat.Subgrid(points=pts[i], weights=w[i], colors=np.full((9, 3), 0.5))
+        p = rsplat.init_position(g)
+        ph, s, _ = rsplat.init_covariance(g, p)
+        pos.append(p)
+        phi.append(ph)
+        scale.append(s)
+    np.savez_compressed(os.path.join(HERE, "subgrids.npz"), points=pts, weights=w,
+                        position=np.array(pos), phi=np.array(phi), scale=np.array(scale))
+
+
+def scan_fixture():
+    """A small 3-frame replay of the reference ingest (store, densify, init).
+
+    Small scene (ground + boxes + spheres seen from close range, 0.2 m voxels)
+    with eta=2e-5 so frames 2 and 3 re-fit ACTIVE voxels from raw ∪ pseudo.
+    """
+    config = PipelineConfig(voxel_size=0.2, eta=2e-5, sensor_var=1e-4,
+                            iterations=0, expansion_threshold=1)
+    sc = scenes.OutdoorScene.make(3, n_boxes=6, n_spheres=6, half=12.0)
+    pipe = MappingPipeline(config)
+    out = {}
+    for fr in range(3):
+        eye = (0.3 * fr, 0.0, 1.8)
+        pos, col = scenes.scan(sc, eye, (eye[0] + 10, 0.0, 1.8), 3, fr,
+                               rays=6000, rows=16, fov_az=np.radians(60.0),
+                               fov_el=np.radians(30.0))
+        cam = Camera(fx=60.0, fy=60.0, cx=39.5, cy=29.5, width=80, height=60,
+                     rotation=scenes.look_at(eye, (eye[0] + 10, 0.0, 1.8))[0],
+                     translation=scenes.look_at(eye, (eye[0] + 10, 0.0, 1.8))[1])
+        pin = scenes.Pinhole(60.0, 60.0, 39.5, 29.5, 80, 60, cam.rotation, cam.translation)
+        image = scenes.render_image(sc, pin)
+        ntr = len(pipe.vmap.transitions)
+        nsolve = len(pipe.vmap.solve_log)
+        ngs = len(pipe.gmap)
+        # capture the update set and predictions exactly as ingest sees them
+        captured = {}
+        orig = rgpr.densify_frame
+
+        def spy(update, vmap, cfg):
+            captured["update"] = list(update)
+            preds = orig(update, vmap, cfg)
+            captured["preds"] = preds
+            return preds
+        import voxsplat.pipeline as rp
+        rp.densify_frame = spy
+        try:
+            pipe.ingest_frame(FrameSample(float(fr), rvm.PointCloud(pos, col, np.zeros(len(pos))),
+                                          image, cam))
+        finally:
+            rp.densify_frame = orig
+        p = f"f{fr}_"
+        out[p + "positions"], out[p + "colors"] = pos, col
+        out[p + "R"], out[p + "t"], out[p + "image"] = cam.rotation, cam.translation, image
+        out[p + "update"] = np.array(captured["update"], dtype=np.int64).reshape(-1, 3)
+        tr = pipe.vmap.transitions[ntr:]
+        out[p + "transitions"] = np.array(
+            [[*t.key, int(t.old), int(t.new)] for t in tr], dtype=np.int64).reshape(-1, 5)
+        preds = captured["preds"]
+        out[p + "pred_keys"] = np.array([pr.key for pr in preds], dtype=np.int64).reshape(-1, 3)
+        out[p + "pred_positions"] = np.stack([pr.positions for pr in preds])
+        out[p + "pred_colors"] = np.stack([pr.colors for pr in preds])
+        out[p + "pred_variances"] = np.stack([pr.variances for pr in preds])
+        out[p + "pred_axis"] = np.array([pipe.vmap.cells[pr.key].value_axis for pr in preds])
+        out[p + "solve_log_len"] = np.array(len(pipe.vmap.solve_log) - nsolve)
+        g = pipe.gmap
+        out[p + "g_positions"] = g.positions[ngs:]
+        out[p + "g_scales"] = g.scales[ngs:]
+        out[p + "g_rotations"] = g.rotations[ngs:]
+        out[p + "g_opacities"] = g.opacities[ngs:]
+        out[p + "g_colors"] = g.colors[ngs:]
+        out[p + "g_source_keys"] = g.source_keys[ngs:]
+    keys = sorted(pipe.vmap.cells)
+    out["final_keys"] = np.array(keys, dtype=np.int64)
+    out["final_counts"] = np.array([pipe.vmap.cells[k].point_count for k in keys])
+    out["final_states"] = np.array([int(pipe.vmap.cells[k].state) for k in keys])
+    out["camera_intrinsics"] = np.array([60.0, 60.0, 39.5, 29.5, 80, 60])
+    out["config"] = np.array([config.voxel_size, config.eta, config.sensor_var,
+                              config.tau, config.kernel_lambda, config.jitter])
+    np.savez_compressed(os.path.join(HERE, "scan_frames.npz"), **out)
+
+
+if __name__ == "__main__":
+    gpr_fixture()
+    keys_fixture()
+    axis_fixture()
+    grids_fixture()
+    subgrid_fixture()
+    scan_fixture()
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
