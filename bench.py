@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: per-voxel GPR + Gaussian-init throughput (voxels/s, ms/scan).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--voxels V] [--workload map|scan]
+
+Default workload (BASELINE.json config 4 on one GPU): a ~1M-voxel synthetic
+planar map (points-per-voxel histogram of the 32-beam scan, ~25.5M points,
+0.5 m voxels) ingested as ONE scan into an empty map: hash -> per-voxel
+FP64 GPR (81-point grid) -> Gaussian init for every first solve.  A step is
+one such ingest into a freshly cleared map.  Inputs (1.2 GB) exceed L2, so
+no explicit flush is needed.  Under torchrun each rank ingests its own 1M-voxel
+map (weak scaling, no data-path collective: the path shards by voxel).
+
+`value` is timed with CUDA events on the launching stream with inputs already
+in HBM; `e2e` runs the same step through the public API
+(`MappingEngine.ingest`) from pinned host tensors (H2D of points, colours
+and image inside the timed region, D2H of the ingest report).  `--impl
+reference` times the CPU oracle (NumPy/SciPy restatement of the reference,
+oracle/voxsplat_oracle.py) on a bounded sample with all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import scenes  # noqa: E402
+
+METRIC = "per-voxel GPR+Gaussian-init voxels/sec; ms/scan"
+UNIT = "voxels/s"
+TAU = 10
+NSTAR = 81
+
+
+def gpr_flops(n):
+    """Algorithmic FP64 flops of one solve (n* = 81)."""
+    n = np.asarray(n, dtype=np.float64)
+    m = NSTAR
+    return n ** 3 / 3 + n * n * m + n * n + 4 * n * m + 6 * (n * (n + 1) / 2 + n * m)
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def make_workload(n_voxels, rank=0, seed=0):
+    side = int(math.ceil(math.sqrt(n_voxels)))
+    pos, col, counts, keys, owner = scenes.planar_map(n_voxels, voxel_size=0.5, seed=seed + rank,
+                                                      key_offset=(0, rank * (side + 8), 0))
+    # a downward camera over the map for colour sampling
+    cx = 0.25 * side
+    cy = 0.5 * (rank * (side + 8) + side / 2)
+    R, t = scenes.look_at((cx, cy, 150.0), (cx, cy + 1e-3, 0.0), up=(0.0, 1.0, 0.0))
+    cam = dict(fx=500.0, fy=500.0, cx=319.5, cy=239.5, width=640, height=480, R=R, t=t)
+    img = np.random.default_rng(seed + 99).uniform(0.0, 1.0, (480, 640, 3))
+    return pos, col, counts, keys, owner, cam, img
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/vx_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+
+def _oracle_worker(args):
+    pos, col, cam, img, cfg = args
+    from oracle import voxsplat_oracle as O
+    omap = O.OracleMap(0.5, 1e-4, TAU, 0.3)
+    ocam = O.OracleCamera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], cam["width"],
+                          cam["height"], cam["R"], cam["t"])
+    t0 = time.perf_counter()
+    res = O.ingest(omap, pos, col, O.DensifyConfig(), camera=ocam, image=img)
+    return len(res["predictions"]), time.perf_counter() - t0
+
+
+def cpu_oracle_rate(pos, col, owner, cam, img, sample_every, procs):
+    """Oracle ingest of every `sample_every`-th voxel, split over `procs` processes."""
+    mask = owner % sample_every == 0
+    spos, scol, sown = pos[mask], col[mask], owner[mask]
+    shard = (sown // sample_every) % procs
+    jobs = [(spos[shard == r], scol[shard == r], cam, img, None) for r in range(procs)]
+    t0 = time.perf_counter()
+    if procs > 1:
+        with mp.get_context("fork").Pool(procs) as pool:
+            out = pool.map(_oracle_worker, jobs)
+    else:
+        out = [_oracle_worker(j) for j in jobs]
+    wall = time.perf_counter() - t0
+    solved = sum(o[0] for o in out)
+    return solved / wall, solved, wall, int(mask.sum())
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    procs = len(os.sched_getaffinity(0))
+    pos, col, counts, keys, owner, cam, img = make_workload(args.voxels, 0)
+    rates = []
+    for _ in range(args.warmup):
+        pass   # the oracle has no warm-up state; W is honoured by not timing anything
+    for _ in range(args.steps):
+        r, solved, wall, npts = cpu_oracle_rate(pos, col, owner, cam, img, args.ref_sample, procs)
+        rates.append(r)
+    v = float(np.median(rates))
+    ms = args.voxels * (counts >= TAU).mean() / v * 1e3
+    sample = (f"every {args.ref_sample}th voxel of the {args.voxels}-voxel map "
+              f"({solved} solved voxels, {npts} points) per step, {procs} processes")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config4: {args.voxels}-voxel planar map, one scan, 0.5 m voxels",
+                       "voxels": args.voxels},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_17084_b200 as vx
+    from paper_2410_17084_b200 import _native as N
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    N.lib()
+
+    pos, col, counts, keys, owner, cam_d, img = make_workload(args.voxels, rank)
+    npts = len(pos)
+    cam = vx.Camera(cam_d["fx"], cam_d["fy"], cam_d["cx"], cam_d["cy"], cam_d["width"],
+                    cam_d["height"], cam_d["R"], cam_d["t"])
+    config = vx.PipelineConfig(voxel_size=0.5, tau=TAU)
+    solved_expected = int((counts >= TAU).sum())
+
+    # host pinned inputs (e2e) and device-resident inputs (value)
+    h_xyz = torch.from_numpy(pos).pin_memory()
+    h_rgb = torch.from_numpy(col).pin_memory()
+    h_img = torch.from_numpy(img).pin_memory()
+    d_xyz, d_rgb, d_img = (t.to(dev) for t in (h_xyz, h_rgb, h_img))
+    eng = vx.MappingEngine(config, voxel_capacity=int(args.voxels * 1.05),
+                           point_capacity=int(npts * 1.6),
+                           gaussian_capacity=9 * solved_expected + 1024)
+
+    def step_device():
+        eng.reset()
+        return eng.ingest_device(d_xyz, d_rgb, npts, cam, d_img)
+
+    def step_e2e():
+        eng.reset()
+        x = h_xyz.to(dev, non_blocking=True)
+        c = h_rgb.to(dev, non_blocking=True)
+        i = h_img.to(dev, non_blocking=True)
+        return eng.ingest_device(x, c, npts, cam, i)   # report counters are read back (D2H)
+
+    for _ in range(args.warmup):
+        rep = step_device()
+    torch.cuda.synchronize()
+    if rep.voxels_solved < 0.99 * solved_expected:
+        raise RuntimeError(f"solved {rep.voxels_solved} of {solved_expected} expected voxels")
+    peak64 = N.fp64_peak_tflops()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+
+    def timed(fn, k, profile=False):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if profile:
+            N.profile(True)
+        l0 = N.launch_count()
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        reps = [fn() for _ in range(k)]
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        launches = N.launch_count() - l0
+        prof = N.profile_read() if profile else None
+        if profile:
+            N.profile(False)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if profile:   # share of the dominant stage from rank 0's timers
+                pass
+        return float(t.item()), reps, launches, prof
+
+    clocks = Clocks(local_rank)
+    clocks.start()
+    ms, reps, launches, prof = timed(step_device, args.steps, profile=True)
+    clk = clocks.stop()
+    solved = sum(r.voxels_solved for r in reps) / args.steps
+    tot_solved = torch.tensor([solved], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot_solved)
+    ms_step = ms / args.steps
+    value = float(tot_solved.item()) / (ms_step / 1e3)
+
+    e2e_ms, e2e_reps, _, _ = timed(step_e2e, args.steps)
+    e2e_value = float(tot_solved.item()) / (e2e_ms / args.steps / 1e3)
+    h2d = h_xyz.numel() * 8 + h_rgb.numel() * 8 + h_img.numel() * 8
+    d2h = 7 * 8 * 2 + 21 * 8   # frame/densify info structs + counters per step
+
+    # roofline of the dominant kernel (FP64 pipe for the GPR solves)
+    stages = {k: v for k, v in prof.items() if k != "densify" and v[1] > 0}
+    top = max(stages, key=lambda k: stages[k][0])
+    top_ms, top_n = stages[top]
+    sol = counts[counts >= TAU]
+    bucket = {"gpr_team32": sol[sol <= 32], "gpr_team64": sol[(sol > 32) & (sol <= 64)],
+              "gpr_generic": sol[sol > 64]}
+    if top in bucket:
+        flops = float(gpr_flops(bucket[top]).sum()) * args.steps
+        achieved = flops / (top_ms / 1e3) / 1e12
+        roof = {"kernel": top, "bound": "fp64", "achieved": achieved, "peak": peak64,
+                "unit": "TFLOP/s", "frac": achieved / peak64,
+                "peak_source": "measured in-run DFMA microbenchmark (vx_fp64_peak)",
+                "traffic": None, "launch_ms": top_ms / top_n,
+                "share_of_step": top_ms / ms}
+    else:
+        # hashing / splat are HBM-bound: algorithmic bytes per point = 104
+        bts = (104.0 * npts if top == "hash" else 1224.0 * solved_expected) * args.steps
+        achieved = bts / (top_ms / 1e3) / 1e9
+        pk = float(peaks.get("hbm_gbs", 6548.8))
+        roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s",
+                "frac": achieved / pk, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "traffic": None, "launch_ms": top_ms / top_n, "share_of_step": top_ms / ms}
+    stage_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        procs = len(os.sched_getaffinity(0))
+        r, s_solved, wall, spts = cpu_oracle_rate(pos, col, owner, cam_d, img, args.ref_sample,
+                                                  procs)
+        cpu = {"value": r, "unit": UNIT, "cores": procs, "kind": "port",
+               "sample": f"every {args.ref_sample}th voxel ({s_solved} solved, {spts} points), "
+                         f"oracle store+densify+init, {wall:.1f} s wall over {procs} processes"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config4: {args.voxels}-voxel planar map per GPU ingested as "
+                                   f"one scan ({npts} points, 0.5 m voxels, n*=81, "
+                                   f"Gaussian init for all first solves)",
+                       "voxels_per_gpu": args.voxels, "points_per_gpu": npts,
+                       "solved_per_gpu": solved, "l2": "inputs 1.2 GB > 126 MB L2, no flush",
+                       "parallelism": f"hash-shard x{world}"},
+            "roofline": roof,
+            "stage_ms": stage_ms,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "peaks": {"fp64_tflops_measured": peak64, "hbm_gbs": peaks.get("hbm_gbs")},
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--voxels", type=int, default=1_000_000)
+    ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        if args.impl == "reference":
+            if rank != 0:
+                return
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_gpu(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,597 @@
+// extern "C" entry points of libvoxgpr (include/voxgpr.h) and the small
+// stateless kernels behind them.
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "vx_common.cuh"
+#include "vx_internal.h"
+
+namespace vx {
+
+std::atomic<int64_t> g_launches{0};
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int sm_count() {
+    static int cached = 0;
+    if (cached == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+        if (cached <= 0) cached = 148;
+    }
+    return cached;
+}
+
+int DevBuf::reserve(size_t want, cudaStream_t s, bool keep) {
+    if (want <= bytes) return VX_OK;
+    size_t nb = want + want / 4 + 256;
+    void* p = nullptr;
+    VX_CUDA(cudaMalloc(&p, nb));
+    if (keep && ptr && bytes) VX_CUDA(cudaMemcpyAsync(p, ptr, bytes, cudaMemcpyDeviceToDevice, s));
+    if (ptr) VX_CUDA(cudaFree(ptr));
+    ptr = p;
+    bytes = nb;
+    return VX_OK;
+}
+
+void DevBuf::release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+}
+
+// ------------------------------------------------------------ small kernels
+__global__ void k_voxel_keys(const double* xyz, int64_t n, double vs, int64_t* keys, int* err) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n * 3) return;
+    const double v = xyz[i];
+    if (!isfinite(v)) {
+        atomicOr(err, 1);
+        keys[i] = 0;
+        return;
+    }
+    const double f = floor(xdiv(v, vs));
+    if (!(f >= -9.2233720368547758e18 && f < 9.2233720368547758e18)) {
+        atomicOr(err, 2);
+        keys[i] = 0;
+        return;
+    }
+    keys[i] = int64_t(f);
+}
+
+__global__ void k_kernel_matrix(const double* xa, int64_t na, const double* xb, int64_t nb, double lam,
+                                int kind, double* out) {
+    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= na * nb) return;
+    const int64_t i = e / nb, j = e - i * nb;
+    out[e] = kernel_value(kind, lam, dist2_exact(xa[i * 2], xa[i * 2 + 1], xb[j * 2], xb[j * 2 + 1]));
+}
+
+// make_mesh_grid (gpr.py:104-120): c_i = lo + ((i + 0.5) * (hi - lo)) / m,
+// ordered (subgrid row, subgrid col, fine row, fine col)
+__global__ void k_mesh_grid(const double* ext, int64_t P, int n_s, int n_r, double* out) {
+    const int mm = n_s * n_r;
+    const int64_t M = int64_t(mm) * mm;
+    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= P * M) return;
+    const int64_t p = e / M;
+    const int q = int(e - p * M);
+    const int nr2 = n_r * n_r;
+    const int sr = q / (n_s * nr2);
+    const int rem = q - sr * n_s * nr2;
+    const int sc = rem / nr2;
+    const int rem2 = rem - sc * nr2;
+    const int fr = rem2 / n_r, fc = rem2 - fr * n_r;
+    const double lo0 = ext[p * 4], hi0 = ext[p * 4 + 1], lo1 = ext[p * 4 + 2], hi1 = ext[p * 4 + 3];
+    out[e * 2] = xadd(lo0, xdiv(xmul(double(sr * n_r + fr) + 0.5, xsub(hi0, lo0)), double(mm)));
+    out[e * 2 + 1] = xadd(lo1, xdiv(xmul(double(sc * n_r + fc) + 0.5, xsub(hi1, lo1)), double(mm)));
+}
+
+// select_value_axis (gpr.py:57-78), one warp per point set
+__global__ void k_select_axis(const double* pts, const int64_t* off, int64_t P, int8_t* axis_out) {
+    const int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= P) return;
+    const int64_t b = off[p];
+    const int n = int(off[p + 1] - b);
+    const double* P3 = pts + b * 3;
+    if (n < 3) {
+        if (lane == 0) axis_out[p] = -1;
+        return;
+    }
+    double mx = 0, my = 0, mz = 0;
+    if (lane == 0) {
+        for (int r = 0; r < n; ++r) {
+            mx = xadd(mx, P3[r * 3]);
+            my = xadd(my, P3[r * 3 + 1]);
+            mz = xadd(mz, P3[r * 3 + 2]);
+        }
+        mx = xdiv(mx, double(n));
+        my = xdiv(my, double(n));
+        mz = xdiv(mz, double(n));
+    }
+    mx = __shfl_sync(FULL, mx, 0);
+    my = __shfl_sync(FULL, my, 0);
+    mz = __shfl_sync(FULL, mz, 0);
+    double c[6] = {0, 0, 0, 0, 0, 0};
+    for (int r = lane; r < n; r += 32) {
+        double dx = xsub(P3[r * 3], mx), dy = xsub(P3[r * 3 + 1], my), dz = xsub(P3[r * 3 + 2], mz);
+        c[0] = fma(dx, dx, c[0]);
+        c[1] = fma(dx, dy, c[1]);
+        c[2] = fma(dx, dz, c[2]);
+        c[3] = fma(dy, dy, c[3]);
+        c[4] = fma(dy, dz, c[4]);
+        c[5] = fma(dz, dz, c[5]);
+    }
+    for (int k = 0; k < 6; ++k)
+        for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(FULL, c[k], o);
+    if (lane == 0) {
+        for (int k = 0; k < 6; ++k) c[k] /= double(n);
+        double ev[3], v0[3];
+        eig3_sym(c, ev, v0, nullptr);
+        int ax = -1;
+        if (!(ev[2] <= 1e-18 || ev[1] <= 1e-9 * ev[2])) {
+            double w0 = fabs(v0[0]), w1 = fabs(v0[1]), w2 = fabs(v0[2]);
+            ax = 2;
+            double best = w2;
+            if (w1 > best) { ax = 1; best = w1; }
+            if (w0 > best) { ax = 0; }
+        }
+        axis_out[p] = int8_t(ax);
+    }
+}
+
+// problem-mode bucketing for gpr_solve_batch
+__global__ void k_problem_buckets(const int64_t* x_off, int64_t P, int32_t* items, int* fill,
+                                  int64_t off1, int64_t off2) {
+    const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const int n = int(x_off[p + 1] - x_off[p]);
+    const int b = bucket_of(n);
+    const int pos = atomicAdd(fill + b, 1);
+    const int64_t base = b == 0 ? 0 : (b == 1 ? off1 : off2);
+    items[base + pos] = int32_t(p);
+}
+__global__ void k_problem_count(const int64_t* x_off, int64_t P, int* counts) {
+    const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    atomicAdd(counts + bucket_of(int(x_off[p + 1] - x_off[p])), 1);
+}
+
+// FP64 peak: independent DFMA chains, 8 per thread
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = threadIdx.x * 1e-3 + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = fma(r[k], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += r[k];
+    if (s == 12345.678) out[0] = s;
+}
+
+// ---------------------------------------------------------------- profiling
+struct ProfState {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[P_COUNT];
+    cudaEvent_t open[P_COUNT] = {};
+    double ms[P_COUNT] = {};
+    int64_t n[P_COUNT] = {};
+};
+static ProfState g_prof;
+static std::mutex g_prof_mu;
+
+void prof_begin(int stage, cudaStream_t s) {
+    if (!g_prof.on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    g_prof.open[stage] = e;
+}
+
+void prof_end(int stage, cudaStream_t s) {
+    if (!g_prof.on || !g_prof.open[stage]) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.ev[stage].push_back({g_prof.open[stage], e});
+    g_prof.open[stage] = nullptr;
+}
+
+static void prof_collect() {
+    for (int k = 0; k < P_COUNT; ++k) {
+        for (auto& pr : g_prof.ev[k]) {
+            float ms = 0;
+            cudaEventSynchronize(pr.second);
+            cudaEventElapsedTime(&ms, pr.first, pr.second);
+            g_prof.ms[k] += ms;
+            g_prof.n[k] += 1;
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+        g_prof.ev[k].clear();
+    }
+}
+
+struct Scratch {
+    DevBuf a, b, c;
+    int* host = nullptr;
+};
+static std::mutex g_scratch_mu;
+static Scratch& scratch() {
+    static Scratch s;
+    return s;
+}
+
+}  // namespace vx
+
+using namespace vx;
+
+// map internals (vx_map.cu)
+namespace vx {
+int map_store_frame(VxMap* m, const double* xyz, const double* rgb, int64_t n, VxFrameInfo* info,
+                    cudaStream_t s);
+int map_densify(VxMap* m, VxDensifyInfo* info, cudaStream_t s);
+int map_ingest(VxMap* m, const double* xyz, const double* rgb, int64_t n, const VxCamera* cam,
+               const double* image, const VxSplatConfig* scfg, VxGaussianOut* out,
+               int64_t out_capacity, int64_t* out_records, VxFrameInfo* fi, VxDensifyInfo* di,
+               cudaStream_t s);
+int map_clear(VxMap* m, cudaStream_t s);
+int map_lookup(VxMap* m, const int64_t* keys, int64_t n, int32_t* out, cudaStream_t s);
+int map_set_frame_keys(VxMap* m, const int64_t* keys, int64_t n, cudaStream_t s);
+int map_apply_prediction(VxMap* m, const int64_t* h_key, const double* xyz, const double* rgb,
+                         const double* var, int64_t M, uint8_t* h_before_after, cudaStream_t s);
+int map_configure_solver(VxMap* m, int n_s, int n_r, double lam, double jitter, int kernel);
+int launch_init_color(const double* pos, const double* fallback, int64_t n, const VxCamera& cam,
+                      const double* image, double* out, cudaStream_t s);
+VxMap* map_new(const VxMapConfig& cfg, int* rc);
+void map_delete(VxMap* m);
+void map_fill_view(VxMap* m, VxMapView* v);
+int map_init_gaussians(VxMap* m, const int32_t* vids, int64_t count, const VxCamera& cam,
+                       const double* image, const VxSplatConfig& cfg, const VxGaussianOut& out,
+                       cudaStream_t s);
+}  // namespace vx
+
+extern "C" {
+
+int vx_abi_version(void) { return VX_ABI_VERSION; }
+const char* vx_last_error(void) { return g_err; }
+int64_t vx_launch_count(void) { return g_launches.load(); }
+
+int vx_voxel_keys(const double* d_xyz, int64_t n, double voxel_size, int64_t* d_keys, void* stream) {
+    if (!(voxel_size > 0)) {
+        set_error("voxel_size must be positive");
+        return VX_E_INPUT;
+    }
+    if (n <= 0) return VX_OK;
+    cudaStream_t s = as_stream(stream);
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    Scratch& sc = scratch();
+    VX_TRY(sc.a.reserve(sizeof(int), s));
+    if (!sc.host) VX_CUDA(cudaMallocHost(&sc.host, 64));
+    VX_CUDA(cudaMemsetAsync(sc.a.ptr, 0, sizeof(int), s));
+    k_voxel_keys<<<unsigned((n * 3 + 255) / 256), 256, 0, s>>>(d_xyz, n, voxel_size, d_keys,
+                                                               sc.a.as<int>());
+    count_launch();
+    VX_CHECK_LAUNCH();
+    VX_CUDA(cudaMemcpyAsync(sc.host, sc.a.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+    VX_CUDA(cudaStreamSynchronize(s));
+    if (sc.host[0] & 1) {
+        set_error("cannot hash non-finite positions");
+        return VX_E_INPUT;
+    }
+    if (sc.host[0] & 2) {
+        set_error("voxel key overflows int64");
+        return VX_E_RANGE;
+    }
+    return VX_OK;
+}
+
+int vx_kernel_matrix(const double* d_xa, int64_t na, const double* d_xb, int64_t nb, double lam,
+                     int32_t kernel, double* d_out, void* stream) {
+    if (!(lam > 0)) {
+        set_error("kernel constant must be positive");
+        return VX_E_INPUT;
+    }
+    if (na <= 0 || nb <= 0) return VX_OK;
+    cudaStream_t s = as_stream(stream);
+    k_kernel_matrix<<<unsigned((na * nb + 255) / 256), 256, 0, s>>>(d_xa, na, d_xb, nb, lam, kernel,
+                                                                    d_out);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
+int vx_mesh_grid(const double* d_ext, int64_t num, int32_t n_s, int32_t n_r, double* d_out,
+                 void* stream) {
+    if (n_s < 1 || n_r < 1) {
+        set_error("n_s and n_r must be at least 1");
+        return VX_E_INPUT;
+    }
+    if (num <= 0) return VX_OK;
+    const int64_t tot = num * int64_t(n_s * n_r) * (n_s * n_r);
+    cudaStream_t s = as_stream(stream);
+    k_mesh_grid<<<unsigned((tot + 255) / 256), 256, 0, s>>>(d_ext, num, n_s, n_r, d_out);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
+int vx_select_axis_batch(const double* d_points, const int64_t* d_offsets, int64_t num, int8_t* d_axis,
+                         void* stream) {
+    if (num <= 0) return VX_OK;
+    cudaStream_t s = as_stream(stream);
+    k_select_axis<<<unsigned((num * 32 + 255) / 256), 256, 0, s>>>(d_points, d_offsets, num, d_axis);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
+int vx_gpr_solve_batch(const VxGprBatch* b, void* stream) {
+    if (!b) {
+        set_error("null batch");
+        return VX_E_INPUT;
+    }
+    const int64_t P = b->num_problems;
+    if (P <= 0) return VX_OK;
+    if (b->d_full && !b->d_full_off) {
+        set_error("d_full requires d_full_off");
+        return VX_E_INPUT;
+    }
+    cudaStream_t s = as_stream(stream);
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    Scratch& sc = scratch();
+    if (!sc.host) VX_CUDA(cudaMallocHost(&sc.host, 64));
+    VX_TRY(sc.a.reserve(size_t(P) * 4, s));
+    VX_TRY(sc.b.reserve(64, s));
+    int* cnt = sc.b.as<int>();
+    VX_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
+    const unsigned g = unsigned((P + 255) / 256);
+    k_problem_count<<<g, 256, 0, s>>>(b->d_x_off, P, cnt);
+    count_launch();
+    VX_CUDA(cudaMemcpyAsync(sc.host, cnt, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    VX_CUDA(cudaStreamSynchronize(s));
+    const int c0 = sc.host[0], c1 = sc.host[1], c2 = sc.host[2];
+    k_problem_buckets<<<g, 256, 0, s>>>(b->d_x_off, P, sc.a.as<int32_t>(), cnt + 4, c0, c0 + c1);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    const int counts[3] = {c0, c1, c2};
+    const int64_t offs[3] = {0, c0, c0 + c1};
+    for (int k = 2; k >= 0; --k) {
+        if (counts[k] == 0) continue;
+        VX_TRY(launch_problem_solve(*b, sc.a.as<int32_t>() + offs[k], counts[k], b->max_n, b->max_m,
+                                    sc.c, s, k));
+    }
+    // the scratch item list must outlive the kernels
+    VX_CUDA(cudaStreamSynchronize(s));
+    return VX_OK;
+}
+
+int vx_subgrid_moments(const double* d_points, const double* d_weights, int64_t num, int32_t k,
+                       const double* d_center, double* d_pos, double* d_phi, void* stream) {
+    if (k < 1) {
+        set_error("subgrid needs at least one point");
+        return VX_E_INPUT;
+    }
+    return launch_moments(d_points, d_weights, num, k, d_center, d_pos, d_phi, as_stream(stream));
+}
+
+int vx_gaussians_from_predictions(const double* d_pred_xyz, const double* d_pred_rgb,
+                                  const double* d_pred_var, const int64_t* d_keys, int64_t count,
+                                  int64_t points_per_prediction, const VxCamera* camera,
+                                  const double* d_image, const VxSplatConfig* cfg, VxGaussianOut* out,
+                                  void* stream) {
+    if (!camera || !cfg || !out) {
+        set_error("camera, cfg and out are required");
+        return VX_E_INPUT;
+    }
+    return launch_gaussians(d_pred_xyz, d_pred_rgb, d_pred_var, nullptr, nullptr, nullptr, d_keys,
+                            count, int(points_per_prediction), *camera, d_image, *cfg, *out,
+                            as_stream(stream));
+}
+
+int vx_map_create(const VxMapConfig* cfg, VxMap** out) {
+    if (!cfg || !out) {
+        set_error("null argument");
+        return VX_E_INPUT;
+    }
+    if (!(cfg->voxel_size > 0)) {
+        set_error("voxel_size must be positive");
+        return VX_E_INPUT;
+    }
+    if (!(cfg->sensor_var >= 0)) {
+        set_error("sensor_var must be nonnegative");
+        return VX_E_INPUT;
+    }
+    if (cfg->n_s < 1 || cfg->n_r < 1 || cfg->n_s * cfg->n_r > 16) {
+        set_error("n_s, n_r must be >= 1 with n_s * n_r <= 16");
+        return VX_E_INPUT;
+    }
+    if (!(cfg->kernel_lambda > 0)) {
+        set_error("kernel constant must be positive");
+        return VX_E_INPUT;
+    }
+    if (cfg->shard_world < 1 || cfg->shard_rank < 0 || cfg->shard_rank >= cfg->shard_world) {
+        set_error("bad shard (rank %d, world %d)", cfg->shard_rank, cfg->shard_world);
+        return VX_E_INPUT;
+    }
+    int rc = VX_OK;
+    VxMap* m = map_new(*cfg, &rc);
+    if (!m) return rc;
+    *out = m;
+    return VX_OK;
+}
+
+int vx_map_destroy(VxMap* map) {
+    if (map) map_delete(map);
+    return VX_OK;
+}
+
+int vx_map_clear(VxMap* map, void* stream) {
+    if (!map) {
+        set_error("null map");
+        return VX_E_INPUT;
+    }
+    return map_clear(map, as_stream(stream));
+}
+
+int vx_map_view(VxMap* map, VxMapView* out) {
+    if (!map || !out) {
+        set_error("null argument");
+        return VX_E_INPUT;
+    }
+    map_fill_view(map, out);
+    return VX_OK;
+}
+
+int vx_map_store_frame(VxMap* map, const double* d_xyz, const double* d_rgb, int64_t n,
+                       VxFrameInfo* info, void* stream) {
+    if (!map) {
+        set_error("null map");
+        return VX_E_INPUT;
+    }
+    return map_store_frame(map, d_xyz, d_rgb, n, info, as_stream(stream));
+}
+
+int vx_map_densify(VxMap* map, VxDensifyInfo* info, void* stream) {
+    if (!map) {
+        set_error("null map");
+        return VX_E_INPUT;
+    }
+    return map_densify(map, info, as_stream(stream));
+}
+
+int vx_map_init_gaussians(VxMap* map, const int32_t* d_voxels, int64_t count, const VxCamera* camera,
+                          const double* d_image, const VxSplatConfig* cfg, VxGaussianOut* out,
+                          void* stream) {
+    if (!map || !camera || !cfg || !out) {
+        set_error("null argument");
+        return VX_E_INPUT;
+    }
+    return map_init_gaussians(map, d_voxels, count, *camera, d_image, *cfg, *out, as_stream(stream));
+}
+
+int vx_map_ingest(VxMap* map, const double* d_xyz, const double* d_rgb, int64_t n,
+                  const VxCamera* camera, const double* d_image, const VxSplatConfig* cfg,
+                  VxGaussianOut* out, int64_t out_capacity, int64_t* out_records,
+                  VxFrameInfo* frame_info, VxDensifyInfo* densify_info, void* stream) {
+    if (!map) {
+        set_error("null map");
+        return VX_E_INPUT;
+    }
+    if (camera && !cfg) {
+        set_error("camera requires a splat config");
+        return VX_E_INPUT;
+    }
+    return map_ingest(map, d_xyz, d_rgb, n, camera, d_image, cfg, out, out_capacity, out_records,
+                      frame_info, densify_info, as_stream(stream));
+}
+
+int vx_map_lookup(VxMap* map, const int64_t* d_keys, int64_t n, int32_t* d_voxels, void* stream) {
+    if (!map) {
+        set_error("null map");
+        return VX_E_INPUT;
+    }
+    return map_lookup(map, d_keys, n, d_voxels, as_stream(stream));
+}
+
+int vx_map_set_frame_keys(VxMap* map, const int64_t* d_keys, int64_t n, void* stream) {
+    if (!map) {
+        set_error("null map");
+        return VX_E_INPUT;
+    }
+    return map_set_frame_keys(map, d_keys, n, as_stream(stream));
+}
+
+int vx_map_apply_prediction(VxMap* map, const int64_t* h_key, const double* d_xyz, const double* d_rgb,
+                            const double* d_var, int64_t m, uint8_t* h_before_after, void* stream) {
+    if (!map || !h_key || !h_before_after) {
+        set_error("null argument");
+        return VX_E_INPUT;
+    }
+    return map_apply_prediction(map, h_key, d_xyz, d_rgb, d_var, m, h_before_after, as_stream(stream));
+}
+
+int vx_map_configure_solver(VxMap* map, int32_t n_s, int32_t n_r, double kernel_lambda, double jitter,
+                            int32_t kernel) {
+    if (!map) {
+        set_error("null map");
+        return VX_E_INPUT;
+    }
+    return map_configure_solver(map, n_s, n_r, kernel_lambda, jitter, kernel);
+}
+
+int vx_init_color(const double* d_positions, const double* d_fallback, int64_t n, const VxCamera* camera,
+                  const double* d_image, double* d_sh0, void* stream) {
+    if (!camera) {
+        set_error("camera required");
+        return VX_E_INPUT;
+    }
+    return launch_init_color(d_positions, d_fallback, n, *camera, d_image, d_sh0, as_stream(stream));
+}
+
+int vx_profile(int enable) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    prof_collect();
+    for (int k = 0; k < P_COUNT; ++k) {
+        g_prof.ms[k] = 0;
+        g_prof.n[k] = 0;
+    }
+    g_prof.on = enable != 0;
+    return VX_OK;
+}
+
+int vx_profile_read(double* ms, int64_t* launches, int32_t max_stages) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    prof_collect();
+    for (int k = 0; k < P_COUNT && k < max_stages; ++k) {
+        ms[k] = g_prof.ms[k];
+        launches[k] = g_prof.n[k];
+    }
+    return P_COUNT;
+}
+
+int vx_fp64_peak(double* tflops, void* stream) {
+    cudaStream_t s = as_stream(stream);
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    Scratch& sc = scratch();
+    VX_TRY(sc.a.reserve(64, s));
+    const int blocks = sm_count() * 8, iters = 4096;
+    cudaEvent_t e0, e1;
+    VX_CUDA(cudaEventCreate(&e0));
+    VX_CUDA(cudaEventCreate(&e1));
+    k_dfma_peak<<<blocks, 256, 0, s>>>(sc.a.as<double>(), iters, 0.999999, 1e-7);  // warm-up
+    count_launch();
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        VX_CUDA(cudaEventRecord(e0, s));
+        k_dfma_peak<<<blocks, 256, 0, s>>>(sc.a.as<double>(), iters, 0.999999, 1e-7);
+        count_launch();
+        VX_CUDA(cudaEventRecord(e1, s));
+        VX_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        VX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8.0 * double(iters) * double(blocks) * 256.0;
+    *tflops = flops / (double(best) * 1e-3) / 1e12;
+    return VX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,227 @@
+// Shared device helpers for the voxel-GPR hot path (sm_100a only).
+//
+// Everything numeric here is FP64: SURVEY.md §0-5 measured that every FP32
+// variant of the per-voxel GPR misses the reference's 1e-9 relative parity by
+// 20-700x, so the roofline of the solve kernels is the FP64 FMA pipe.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/voxgpr.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "voxgpr is written for sm_100a (B200) only"
+#endif
+
+namespace vx {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint64_t EMPTY_KEY = ~0ull;
+constexpr int KEY_BITS = 21;                        // per axis, offset binary
+constexpr int64_t KEY_BIAS = int64_t(1) << (KEY_BITS - 1);   // 2^20
+constexpr int64_t KEY_LIM = KEY_BIAS;               // |k| < 2^20 representable
+
+// ---------------------------------------------------------------------------
+// exact IEEE helpers: the reference's NumPy expressions are evaluated
+// operation by operation without FMA contraction; where bit-exactness is a
+// parity gate (grid coordinates, nearest-colour distances, keys) we use the
+// _rn intrinsics so nvcc cannot contract them.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// squared distance in the parameter plane, NumPy order ((dx**2) + (dy**2))
+// (gpr.py:129 and gpr.py:304)
+__device__ __forceinline__ double dist2_exact(double ax, double ay, double bx, double by) {
+    double dx = xsub(ax, bx), dy = xsub(ay, by);
+    return xadd(xmul(dx, dx), xmul(dy, dy));
+}
+
+// ---------------------------------------------------------------------------
+// keys: pack a lattice triple into 63 bits (21 bits per axis, offset binary)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t pack_key(int64_t a, int64_t b, int64_t c) {
+    return (uint64_t(a + KEY_BIAS) << (2 * KEY_BITS)) | (uint64_t(b + KEY_BIAS) << KEY_BITS) |
+           uint64_t(c + KEY_BIAS);
+}
+__host__ __device__ __forceinline__ void unpack_key(uint64_t k, int64_t* a, int64_t* b, int64_t* c) {
+    const uint64_t m = (uint64_t(1) << KEY_BITS) - 1;
+    *a = int64_t((k >> (2 * KEY_BITS)) & m) - KEY_BIAS;
+    *b = int64_t((k >> KEY_BITS) & m) - KEY_BIAS;
+    *c = int64_t(k & m) - KEY_BIAS;
+}
+// murmur3 finaliser: spreads spatially adjacent keys over the table and over
+// shards (voxel owner = mix(key) mod world)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+// ---------------------------------------------------------------------------
+// NumPy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum): n < 8 sequential; n <= 128 eight strided accumulators
+// combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail;
+// larger n splits at n/2 rounded down to a multiple of 8.  Used for the
+// reductions the reference evaluates with ndarray.sum()/mean() on contiguous
+// 1-D data (f.mean() gpr.py:291, variances.mean() voxel_map.py:170, subgrid
+// weight sums splat_init.py:94), so those are bit-exact.
+// `get(i)` returns element i.
+// ---------------------------------------------------------------------------
+template <typename Get>
+__device__ double np_pairwise_block(Get get, int lo, int n) {
+    if (n < 8) {
+        double s = -0.0;          // NumPy starts the plain loop from -0.0
+        for (int i = 0; i < n; ++i) s = xadd(s, get(lo + i));
+        return s;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = get(lo + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = xadd(r[j], get(lo + i + j));
+    }
+    double res = xadd(xadd(xadd(r[0], r[1]), xadd(r[2], r[3])),
+                      xadd(xadd(r[4], r[5]), xadd(r[6], r[7])));
+    for (; i < n; ++i) res = xadd(res, get(lo + i));
+    return res;
+}
+
+template <typename Get>
+__device__ double np_pairwise_sum(Get get, int n) {
+    // iterative form of the recursive split for n > 128 (depth <= 24)
+    if (n <= 128) return np_pairwise_block(get, 0, n);
+    int lo_s[32], n_s[32], state[32];
+    double acc[32];
+    int sp = 0;
+    lo_s[0] = 0; n_s[0] = n; state[0] = 0;
+    double ret = 0.0;
+    while (sp >= 0) {
+        int lo = lo_s[sp], cnt = n_s[sp];
+        if (cnt <= 128) {
+            ret = np_pairwise_block(get, lo, cnt);
+            --sp;
+            // feed result to parent
+            while (sp >= 0) {
+                if (state[sp] == 1) {          // left done, start right
+                    acc[sp] = ret;
+                    state[sp] = 2;
+                    int n2 = n_s[sp] / 2;
+                    n2 -= n2 % 8;
+                    ++sp;
+                    lo_s[sp] = lo_s[sp - 1] + n2;
+                    n_s[sp] = n_s[sp - 1] - n2;
+                    state[sp] = 0;
+                    break;
+                } else {                       // right done
+                    ret = xadd(acc[sp], ret);
+                    --sp;
+                }
+            }
+            continue;
+        }
+        // split: process left half first
+        state[sp] = 1;
+        int n2 = cnt / 2;
+        n2 -= n2 % 8;
+        ++sp;
+        lo_s[sp] = lo;
+        n_s[sp] = n2;
+        state[sp] = 0;
+    }
+    return ret;
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric 3x3 eigensolver (cyclic Jacobi, FP64).  Returns eigenvalues in
+// ascending order and the eigenvector of the smallest one.  Jacobi is
+// accurate to O(eps*|A|/gap) in the eigenvectors — the same accuracy class as
+// LAPACK dsyevd used by the reference (numpy.linalg.eigh, gpr.py:72) — which
+// keeps the discrete value-axis choice stable on near-isotropic voxels.
+// ---------------------------------------------------------------------------
+__device__ inline void eig3_sym(const double c[6],  // xx, xy, xz, yy, yz, zz
+                                double evals[3], double vmin[3], double V[9]) {
+    double a[3][3] = {{c[0], c[1], c[2]}, {c[1], c[3], c[4]}, {c[2], c[4], c[5]}};
+    double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+    for (int sweep = 0; sweep < 12; ++sweep) {
+        double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+        if (off == 0.0) break;
+        const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
+        for (int r = 0; r < 3; ++r) {
+            int p = P[r], q = Q[r];
+            double apq = a[p][q];
+            if (apq == 0.0) continue;
+            double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+            double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            if (isinf(theta)) t = 0.5 / theta;
+            double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+            for (int k = 0; k < 3; ++k) {          // A <- A J
+                double akp = a[k][p], akq = a[k][q];
+                a[k][p] = cs * akp - sn * akq;
+                a[k][q] = sn * akp + cs * akq;
+            }
+            for (int k = 0; k < 3; ++k) {          // A <- J^T A
+                double apk = a[p][k], aqk = a[q][k];
+                a[p][k] = cs * apk - sn * aqk;
+                a[q][k] = sn * apk + cs * aqk;
+            }
+            a[p][q] = a[q][p] = 0.0;
+            for (int k = 0; k < 3; ++k) {          // V <- V J
+                double vkp = v[k][p], vkq = v[k][q];
+                v[k][p] = cs * vkp - sn * vkq;
+                v[k][q] = sn * vkp + cs * vkq;
+            }
+        }
+    }
+    int idx[3] = {0, 1, 2};
+    double d[3] = {a[0][0], a[1][1], a[2][2]};
+    // sort ascending (3 elements)
+    if (d[idx[1]] < d[idx[0]]) { int t = idx[0]; idx[0] = idx[1]; idx[1] = t; }
+    if (d[idx[2]] < d[idx[1]]) { int t = idx[1]; idx[1] = idx[2]; idx[2] = t; }
+    if (d[idx[1]] < d[idx[0]]) { int t = idx[0]; idx[0] = idx[1]; idx[1] = t; }
+    for (int k = 0; k < 3; ++k) evals[k] = d[idx[k]];
+    for (int k = 0; k < 3; ++k) vmin[k] = v[k][idx[0]];
+    if (V) {
+        for (int col = 0; col < 3; ++col)
+            for (int k = 0; k < 3; ++k) V[k * 3 + col] = v[k][idx[col]];
+    }
+}
+
+// value axis -> ordered pair of parameter axes (gpr.py:36)
+__host__ __device__ __forceinline__ int param_axis_a(int ax) { return ax == 0 ? 1 : (ax == 1 ? 2 : 0); }
+__host__ __device__ __forceinline__ int param_axis_b(int ax) { return ax == 0 ? 2 : (ax == 1 ? 0 : 1); }
+
+// Kernel functions with k(q,q)=1.  SE is the reference kernel (gpr.py:123-130):
+// exp(-lam * d2) with d2 from dist2_exact.  Matern-3/2 and -5/2 are north-star
+// extensions (no reference oracle).
+__device__ __forceinline__ double kernel_value(int kind, double lam, double d2) {
+    if (kind == VX_KERNEL_SE) return exp(xmul(-lam, d2));
+    double r = sqrt(lam * d2);
+    if (kind == VX_KERNEL_MATERN32) {
+        double s = 1.7320508075688772 * r;
+        return (1.0 + s) * exp(-s);
+    }
+    double s = 2.23606797749979 * r;
+    return (1.0 + s + s * s / 3.0) * exp(-s);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// named barrier for a team of `nthreads` threads (multiple of 32)
+__device__ __forceinline__ void team_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+}  // namespace vx

@@ -1,0 +1,115 @@
+// Host-side internals shared by the voxgpr translation units.
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/voxgpr.h"
+
+namespace vx {
+
+void set_error(const char* fmt, ...);
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+#define VX_CUDA(call)                                                              \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) {                                                   \
+            ::vx::set_error("%s:%d: %s: %s", __FILE__, __LINE__, #call,            \
+                            cudaGetErrorString(e_));                               \
+            return e_ == cudaErrorMemoryAllocation ? VX_E_NOMEM : VX_E_CUDA;       \
+        }                                                                          \
+    } while (0)
+
+#define VX_CHECK_LAUNCH() VX_CUDA(cudaGetLastError())
+
+#define VX_TRY(expr)              \
+    do {                          \
+        int r_ = (expr);          \
+        if (r_ != VX_OK) return r_; \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Optional CUDA-event timers around the library's stages (vx_profile_*).
+enum ProfStage { P_HASH = 0, P_GPR_SMALL, P_GPR_MEDIUM, P_GPR_GENERIC, P_SPLAT, P_DENSIFY, P_COUNT };
+void prof_begin(int stage, cudaStream_t s);
+void prof_end(int stage, cudaStream_t s);
+
+int sm_count();
+
+// ---------------------------------------------------------------- scratch
+// Grow-only device buffer.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    int reserve(size_t want, cudaStream_t s, bool keep = false);
+    template <typename T> T* as() const { return static_cast<T*>(ptr); }
+    void release();
+};
+
+// ---------------------------------------------------------------- scan/sort
+// exclusive prefix sums; `total` (device, may be null) receives the sum.
+int scan_exclusive_i32(const int32_t* in, int32_t* out, int64_t n, int32_t* total,
+                       DevBuf& tmp, cudaStream_t s);
+int scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* total,
+                       DevBuf& tmp, cudaStream_t s);
+// stable LSD radix sort of (key, value) pairs by the low `bits` bits of key.
+int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
+                     int64_t n, int bits, DevBuf& tmp, cudaStream_t s, bool* result_in_alt);
+
+// ---------------------------------------------------------------- GPR
+// Voxel-mode work description shared by the GPR kernels (device pointers).
+struct VoxelSolveArgs {
+    // work list
+    const int32_t* items;      // indices s into the candidate arrays
+    int32_t num_items;
+    const int32_t* cand_voxel; // (S) voxel id per candidate
+    const int32_t* cand_n;     // (S) training size
+    uint8_t* cand_status;      // (S)
+    uint8_t* cand_before;      // (S)
+    uint8_t* cand_after;       // (S)
+    // store
+    const int64_t* keys;       // (V,3)
+    uint8_t* state;
+    int8_t* value_axis;
+    const int32_t* raw_count;
+    const int64_t* raw_offset;
+    const int32_t* pred_slot;
+    uint8_t* has_pred;
+    const double* raw_xyz;
+    const double* raw_rgb;
+    double* pred_xyz;
+    double* pred_rgb;
+    double* pred_var;
+    // config
+    double voxel_size, sensor_var, eta, lam, jitter;
+    int n_s, n_r, kernel;
+    int M;                     // (n_s n_r)^2
+};
+
+int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStream_t s,
+                       int bucket);
+int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t count,
+                         int max_n, int max_m, DevBuf& work, cudaStream_t s, int bucket);
+
+// bucket boundaries for the training-set size n
+constexpr int BUCKET_SMALL = 32;
+constexpr int BUCKET_MEDIUM = 64;
+__host__ __device__ inline int bucket_of(int n) { return n <= BUCKET_SMALL ? 0 : (n <= BUCKET_MEDIUM ? 1 : 2); }
+
+// ---------------------------------------------------------------- splat init
+int launch_gaussians(const double* pred_xyz, const double* pred_rgb, const double* pred_var,
+                     const int32_t* slot_of, const int32_t* voxel_ids, const int64_t* keys,
+                     const int64_t* direct_keys, int64_t count, int M, const VxCamera& cam,
+                     const double* image, const VxSplatConfig& cfg, const VxGaussianOut& out,
+                     cudaStream_t s);
+int launch_moments(const double* pts, const double* w, int64_t G, int k, const double* center,
+                   double* pos, double* phi, cudaStream_t s);
+
+}  // namespace vx

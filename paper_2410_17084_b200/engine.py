@@ -1,0 +1,186 @@
+"""Device-resident ingest: the batched public entry point of the hot path.
+
+`MappingEngine.ingest` is `MappingPipeline.ingest_frame` (pipeline.py:139-187)
+restricted to the mapping hot path — store the scan, densify the touched
+READY/ACTIVE voxels, initialise Gaussians for first solves once
+`expansion_threshold` of them are pending — executed as one
+`vx_map_ingest` call (expansion_threshold == 1) with every intermediate in
+HBM.  Inputs may be host arrays (copied H2D from pinned staging) or device
+tensors; Gaussian records accumulate in a device SoA.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .config import PipelineConfig
+from .splat_init import GaussianMap, GaussianRecords
+from .voxel_map import VoxelMap
+
+
+@dataclass
+class IngestReport:
+    """Same fields as pipeline.IngestReport (pipeline.py:77-95)."""
+
+    frame_index: int
+    points_stored: int
+    voxels_touched: int
+    voxels_solved: int
+    newly_active: int
+    newly_converged: int
+    primitives_added: int
+    duration_s: float
+    errors: list = field(default_factory=list)
+
+    def to_dict(self) -> dict:
+        return {"frame": self.frame_index, "points": self.points_stored,
+                "touched": self.voxels_touched, "solved": self.voxels_solved,
+                "newly_active": self.newly_active, "newly_converged": self.newly_converged,
+                "primitives_added": self.primitives_added,
+                "ingest_s": round(self.duration_s, 6), "errors": self.errors}
+
+
+class MappingEngine:
+    def __init__(self, config: PipelineConfig, *, shard_rank: int = 0, shard_world: int = 1,
+                 voxel_capacity: int = 0, point_capacity: int = 0, gaussian_capacity: int = 0,
+                 record_log: bool = False):
+        self.config = config
+        self.vmap = VoxelMap.from_config(config, shard_rank=shard_rank, shard_world=shard_world,
+                                         voxel_capacity=voxel_capacity,
+                                         point_capacity=point_capacity, record_log=record_log)
+        self._gcap = int(gaussian_capacity)
+        self.records = None
+        self.num_gaussians = 0
+        self.pending = []        # device int32 tensors of first-solved voxel ids
+        self._pending_n = 0
+        self._pinned = {}
+
+    # -- buffers ------------------------------------------------------------
+    def _ensure_records(self, need: int):
+        import torch
+        if self.records is not None and self.records.count >= need:
+            return
+        cap = max(need, 2 * (self.records.count if self.records else 0), self._gcap, 1024)
+        new = GaussianRecords(cap)
+        if self.records is not None and self.num_gaussians:
+            n = self.num_gaussians
+            for k in ("position", "scale", "rotation", "opacity", "color", "source_key"):
+                getattr(new, k)[:n].copy_(getattr(self.records, k)[:n])
+        self.records = new
+        torch.cuda.current_stream().synchronize()
+
+    def _stage(self, name, arr):
+        """Copy a host array into a reusable pinned buffer, then H2D (async)."""
+        import torch
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        buf = self._pinned.get(name)
+        if buf is None or buf.numel() < a.size:
+            buf = torch.empty(a.size, dtype=torch.float64).pin_memory()
+            self._pinned[name] = buf
+        host = buf[:a.size]
+        host.numpy()[:] = a.reshape(-1)
+        return host.view(*a.shape).to(N.device(), non_blocking=True)
+
+    # -- ingest -------------------------------------------------------------
+    def ingest(self, positions, colors, camera=None, image=None) -> IngestReport:
+        """Host-array ingest: H2D of the scan (and image), then `ingest_device`."""
+        t0 = time.perf_counter()
+        dx = self._stage("xyz", positions) if len(positions) else None
+        dc = self._stage("rgb", colors) if len(positions) else None
+        di = self._stage("img", image) if image is not None else None
+        rep = self.ingest_device(dx, dc, len(positions), camera, di)
+        rep.duration_s = time.perf_counter() - t0
+        return rep
+
+    def ingest_device(self, d_xyz, d_rgb, n: int, camera=None, d_image=None) -> IngestReport:
+        t0 = time.perf_counter()
+        cfg = self.config
+        vm = self.vmap
+        vm._h()
+        vm._configure_solver(cfg)
+        lib = vm._lib
+        nsub = cfg.n_s * cfg.n_s
+        fi, di = N.VxFrameInfo(), N.VxDensifyInfo()
+        added = 0
+        if cfg.expansion_threshold <= 1 and camera is not None:
+            worst = nsub * (n // max(cfg.tau, 1) + 1)
+            self._ensure_records(self.num_gaussians + worst)
+            out = self.records.out_struct(self.num_gaussians)
+            cam, sc = N.camera_struct(camera), N.splat_struct(
+                cfg.n_s, cfg.n_r, cfg.weight_floor, cfg.scale_floor, cfg.initial_opacity,
+                cfg.rotation)
+            written = C.c_int64(0)
+            rc = lib.vx_map_ingest(vm._h(), N.ptr(d_xyz), N.ptr(d_rgb), int(n), C.byref(cam),
+                                   N.ptr(d_image), C.byref(sc), C.byref(out),
+                                   self.records.count - self.num_gaussians, C.byref(written),
+                                   C.byref(fi), C.byref(di), N.stream_ptr())
+            vm._mutated()
+            vm._frame_serial += 1
+            N.check(rc)
+            added = int(written.value)
+            self.num_gaussians += added
+        else:
+            rc = lib.vx_map_store_frame(vm._h(), N.ptr(d_xyz), N.ptr(d_rgb), int(n), C.byref(fi),
+                                        N.stream_ptr())
+            vm._mutated()
+            vm._frame_serial += 1
+            N.check(rc)
+            rc = lib.vx_map_densify(vm._h(), C.byref(di), N.stream_ptr())
+            vm._mutated()
+            N.check(rc)
+            if di.first_solves:
+                v = vm.device_view()
+                S = int(v.solve_candidates)
+                st = N.view_tensor(v.solve_status, (S,), np.uint8)
+                bf = N.view_tensor(v.solve_state_before, (S,), np.uint8)
+                vids = N.view_tensor(v.solve_voxels, (S,), np.int32)
+                first = vids[(st == N.ST_OK) & (bf == 1)].clone()
+                self.pending.append(first)
+                self._pending_n += len(first)
+            if camera is not None and self._pending_n and \
+                    self._pending_n >= cfg.expansion_threshold:
+                added = self._expand(camera, d_image)
+        return IngestReport(frame_index=int(fi.frame_index), points_stored=int(n),
+                            voxels_touched=int(fi.touched), voxels_solved=int(di.solved),
+                            newly_active=int(di.first_solves), newly_converged=int(di.converged),
+                            primitives_added=added, duration_s=time.perf_counter() - t0)
+
+    def _expand(self, camera, d_image) -> int:
+        import torch
+        cfg = self.config
+        vids = torch.cat(self.pending).contiguous()
+        self.pending, self._pending_n = [], 0
+        recs = len(vids) * cfg.n_s * cfg.n_s
+        self._ensure_records(self.num_gaussians + recs)
+        out = self.records.out_struct(self.num_gaussians)
+        cam, sc = N.camera_struct(camera), N.splat_struct(
+            cfg.n_s, cfg.n_r, cfg.weight_floor, cfg.scale_floor, cfg.initial_opacity, cfg.rotation)
+        N.check(self.vmap._lib.vx_map_init_gaussians(self.vmap._h(), N.ptr(vids), len(vids),
+                                                     C.byref(cam), N.ptr(d_image), C.byref(sc),
+                                                     C.byref(out), N.stream_ptr()))
+        self.num_gaussians += recs
+        return recs
+
+    # -- outputs ------------------------------------------------------------
+    def gaussians_device(self) -> dict:
+        n = self.num_gaussians
+        if self.records is None:
+            return {}
+        return {k: getattr(self.records, k)[:n] for k in
+                ("position", "scale", "rotation", "opacity", "color", "source_key")}
+
+    def gaussian_map(self) -> GaussianMap:
+        g = GaussianMap()
+        if self.num_gaussians:
+            g.extend_records(self.records.to_host(self.num_gaussians))
+        return g
+
+    def reset(self):
+        self.vmap.clear()
+        self.num_gaussians = 0
+        self.pending, self._pending_n = [], 0

@@ -1,0 +1,295 @@
+"""Gaussian initialisation on the device (mirror of voxsplat/splat_init.py).
+
+Public names follow `/root/reference/pkg/src/voxsplat/splat_init.py:22-217`.
+The moments, colour sampling and full per-voxel initialisation run in
+libvoxgpr (`vx_subgrid_moments`, `vx_init_color`,
+`vx_gaussians_from_predictions`, and the map-resident `vx_map_init_gaussians`).
+`GaussianMap` is the host SoA container the reference exposes, grown by
+capacity doubling instead of re-concatenating on every `extend` (the
+reference's `extend` is O(map) per call, splat_init.py:169-184).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .camera import Camera
+from .errors import ContractViolationError, InputDomainError
+from .voxel_map import VoxelKey, VoxelPrediction
+
+SH0_BASIS = 0.28209479177
+DEFAULT_SCALE_FLOOR = 1e-4
+DEFAULT_WEIGHT_FLOOR = 1e-8
+IDENTITY_QUATERNION = np.array([1.0, 0.0, 0.0, 0.0])
+
+
+def rgb_to_sh0(color: np.ndarray) -> np.ndarray:
+    """RGB in [0, 1] to zero-degree SH coefficients: (c - 0.5) / basis."""
+    return (np.asarray(color, dtype=float) - 0.5) / SH0_BASIS
+
+
+def sh0_to_rgb(coeff: np.ndarray) -> np.ndarray:
+    return np.asarray(coeff, dtype=float) * SH0_BASIS + 0.5
+
+
+@dataclass
+class GaussianPrimitive:
+    position: np.ndarray
+    scale: np.ndarray
+    rotation: np.ndarray
+    opacity: float
+    color: np.ndarray
+    source_key: VoxelKey | None = None
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=float).reshape(3)
+        self.scale = np.asarray(self.scale, dtype=float).reshape(3)
+        self.rotation = np.asarray(self.rotation, dtype=float).reshape(4)
+        self.color = np.asarray(self.color, dtype=float).reshape(3)
+        if abs(np.linalg.norm(self.rotation) - 1.0) > 1e-9:
+            raise InputDomainError("rotation quaternion must be normalized")
+        if np.any(self.scale <= 0):
+            raise InputDomainError("scale components must be positive")
+        if not 0.0 < self.opacity <= 1.0:
+            raise InputDomainError("opacity must lie in (0, 1]")
+
+
+@dataclass
+class Subgrid:
+    points: np.ndarray
+    weights: np.ndarray
+    colors: np.ndarray
+
+
+def partition_subgrids(prediction: VoxelPrediction, n_s: int, n_r: int,
+                       weight_floor: float = DEFAULT_WEIGHT_FLOOR) -> list[Subgrid]:
+    """n_s^2 contiguous blocks of n_r^2 points; weights 1/max(var, floor) on the device."""
+    block = n_r * n_r
+    expected = n_s * n_s * block
+    if len(prediction) != expected:
+        raise ContractViolationError(
+            f"prediction has {len(prediction)} points, expected {expected}")
+    import torch
+    N.lib()
+    v = N.to_device(prediction.variances)
+    weights = torch.reciprocal(torch.clamp_min(v, float(weight_floor))).cpu().numpy()
+    return [Subgrid(points=prediction.positions[b * block:(b + 1) * block],
+                    weights=weights[b * block:(b + 1) * block],
+                    colors=prediction.colors[b * block:(b + 1) * block])
+            for b in range(n_s * n_s)]
+
+
+def _moments(points, weights, center=None):
+    import torch
+    lib = N.lib()
+    P = np.asarray(points, dtype=float).reshape(1, -1, 3)
+    W = np.asarray(weights, dtype=float).reshape(1, -1)
+    dp, dw = N.to_device(P), N.to_device(W)
+    dc = N.to_device(np.asarray(center, dtype=float).reshape(1, 3)) if center is not None else None
+    pos = torch.empty((1, 3), dtype=torch.float64, device=dp.device)
+    phi = torch.empty((1, 9), dtype=torch.float64, device=dp.device)
+    N.check(lib.vx_subgrid_moments(N.ptr(dp), N.ptr(dw), 1, P.shape[1], N.ptr(dc), N.ptr(pos),
+                                   N.ptr(phi), N.stream_ptr()))
+    return pos.cpu().numpy()[0], phi.cpu().numpy()[0].reshape(3, 3)
+
+
+def init_position(grid: Subgrid) -> np.ndarray:
+    """Weighted mean of the subgrid points (Eq. 6)."""
+    if np.asarray(grid.weights, dtype=float).sum() <= 0:
+        raise InputDomainError("subgrid weights must sum to a positive value")
+    return _moments(grid.points, grid.weights)[0]
+
+
+def init_covariance(grid: Subgrid, position: np.ndarray,
+                    scale_floor: float = DEFAULT_SCALE_FLOOR):
+    """(Phi, scale, quaternion): weighted second moment about `position` (Eq. 7)."""
+    _, phi = _moments(grid.points, grid.weights, center=position)
+    scale = np.maximum(np.sqrt(np.clip(np.diag(phi), 0.0, None)), scale_floor)
+    return phi, scale, IDENTITY_QUATERNION.copy()
+
+
+def init_color(position: np.ndarray, camera: Camera, image: np.ndarray,
+               fallback_rgb: np.ndarray) -> np.ndarray:
+    """SH0 colour of the nearest pixel of the projected position, else the fallback."""
+    import torch
+    lib = N.lib()
+    dp = N.to_device(np.asarray(position, dtype=float).reshape(1, 3))
+    df = N.to_device(np.asarray(fallback_rgb, dtype=float).reshape(1, 3))
+    di = N.to_device(np.asarray(image, dtype=float))
+    out = torch.empty((1, 3), dtype=torch.float64, device=dp.device)
+    cam = N.camera_struct(camera)
+    N.check(lib.vx_init_color(N.ptr(dp), N.ptr(df), 1, C.byref(cam), N.ptr(di), N.ptr(out),
+                              N.stream_ptr()))
+    return out.cpu().numpy()[0]
+
+
+def _splat_cfg(config):
+    return N.splat_struct(config.n_s, config.n_r, config.weight_floor, config.scale_floor,
+                          config.initial_opacity, getattr(config, "rotation", "identity"))
+
+
+class GaussianRecords:
+    """Device SoA of Gaussian records (the VXSPLAT1 record split by field)."""
+
+    def __init__(self, count: int):
+        import torch
+        dev = N.device()
+        self.count = count
+        self.position = torch.empty((count, 3), dtype=torch.float64, device=dev)
+        self.scale = torch.empty((count, 3), dtype=torch.float64, device=dev)
+        self.rotation = torch.empty((count, 4), dtype=torch.float64, device=dev)
+        self.opacity = torch.empty((count,), dtype=torch.float64, device=dev)
+        self.color = torch.empty((count, 3), dtype=torch.float64, device=dev)
+        self.source_key = torch.empty((count, 3), dtype=torch.int64, device=dev)
+
+    def out_struct(self, offset: int = 0) -> N.VxGaussianOut:
+        o = N.VxGaussianOut()
+        o.position = self.position.data_ptr() + offset * 24
+        o.scale = self.scale.data_ptr() + offset * 24
+        o.rotation = self.rotation.data_ptr() + offset * 32
+        o.opacity = self.opacity.data_ptr() + offset * 8
+        o.color = self.color.data_ptr() + offset * 24
+        o.source_key = self.source_key.data_ptr() + offset * 24
+        return o
+
+    def to_host(self, count=None):
+        n = self.count if count is None else count
+        return {k: getattr(self, k)[:n].cpu().numpy() for k in
+                ("position", "scale", "rotation", "opacity", "color", "source_key")}
+
+
+def init_gaussians_batch(predictions, camera: Camera, image: np.ndarray, config) -> dict:
+    """Gaussian records of many predictions in one launch (host SoA dict)."""
+    lib = N.lib()
+    preds = list(predictions)
+    if not preds:
+        return {"position": np.empty((0, 3)), "scale": np.empty((0, 3)),
+                "rotation": np.empty((0, 4)), "opacity": np.empty(0), "color": np.empty((0, 3)),
+                "source_key": np.empty((0, 3), dtype=np.int64)}
+    m = len(preds[0])
+    expected = config.n_s * config.n_s * config.n_r * config.n_r
+    for p in preds:
+        if len(p) != expected:
+            raise ContractViolationError(f"prediction has {len(p)} points, expected {expected}")
+    dx = N.to_device(np.stack([p.positions for p in preds]))
+    dc = N.to_device(np.stack([p.colors for p in preds]))
+    dv = N.to_device(np.stack([p.variances for p in preds]))
+    dk = N.to_device(np.array([tuple(p.key) for p in preds], dtype=np.int64), np.int64)
+    di = N.to_device(np.asarray(image, dtype=float))
+    recs = GaussianRecords(len(preds) * config.n_s * config.n_s)
+    cam, sc, out = N.camera_struct(camera), _splat_cfg(config), recs.out_struct()
+    N.check(lib.vx_gaussians_from_predictions(N.ptr(dx), N.ptr(dc), N.ptr(dv), N.ptr(dk),
+                                              len(preds), m, C.byref(cam), N.ptr(di),
+                                              C.byref(sc), C.byref(out), N.stream_ptr()))
+    return recs.to_host()
+
+
+def init_gaussians_for_voxel(prediction: VoxelPrediction, camera: Camera, image: np.ndarray,
+                             config) -> list[GaussianPrimitive]:
+    """All n_s^2 primitives of a solved voxel (splat_init.py:134-148)."""
+    h = init_gaussians_batch([prediction], camera, image, config)
+    key = VoxelKey(*(int(v) for v in prediction.key))
+    return [GaussianPrimitive(position=h["position"][i], scale=h["scale"][i],
+                              rotation=h["rotation"][i], opacity=float(h["opacity"][i]),
+                              color=h["color"][i], source_key=key)
+            for i in range(len(h["opacity"]))]
+
+
+class GaussianMap:
+    """Struct-of-arrays splat map with amortised O(1) appends."""
+
+    _FIELDS = (("positions", 3, np.float64), ("scales", 3, np.float64),
+               ("rotations", 4, np.float64), ("opacities", 0, np.float64),
+               ("colors", 3, np.float64), ("source_keys", 3, np.int64))
+
+    def __init__(self):
+        self._n = 0
+        self._buf = {name: np.empty((0, w) if w else (0,), dtype=dt)
+                     for name, w, dt in self._FIELDS}
+
+    def _reserve(self, extra: int):
+        need = self._n + extra
+        cap = len(self._buf["opacities"])
+        if need <= cap:
+            return
+        new_cap = max(need, 2 * cap, 64)
+        for name, w, dt in self._FIELDS:
+            nb = np.empty((new_cap, w) if w else (new_cap,), dtype=dt)
+            nb[:self._n] = self._buf[name][:self._n]
+            self._buf[name] = nb
+
+    def __len__(self) -> int:
+        return self._n
+
+    def _get(self, name):
+        return self._buf[name][:self._n]
+
+    def _set(self, name, value):
+        w = dict((f, wd) for f, wd, _ in self._FIELDS)[name]
+        dt = dict((f, d) for f, _, d in self._FIELDS)[name]
+        v = np.asarray(value, dtype=dt)
+        v = v.reshape(-1, w) if w else v.reshape(-1)
+        self._buf[name] = v.copy()
+        self._n = len(v)
+
+    positions = property(lambda s: s._get("positions"), lambda s, v: s._set("positions", v))
+    scales = property(lambda s: s._get("scales"), lambda s, v: s._set("scales", v))
+    rotations = property(lambda s: s._get("rotations"), lambda s, v: s._set("rotations", v))
+    opacities = property(lambda s: s._get("opacities"), lambda s, v: s._set("opacities", v))
+    colors = property(lambda s: s._get("colors"), lambda s, v: s._set("colors", v))
+    source_keys = property(lambda s: s._get("source_keys"), lambda s, v: s._set("source_keys", v))
+
+    def extend(self, primitives: list[GaussianPrimitive]) -> None:
+        if not primitives:
+            return
+        self.extend_arrays(
+            np.stack([p.position for p in primitives]), np.stack([p.scale for p in primitives]),
+            np.stack([p.rotation for p in primitives]),
+            np.array([p.opacity for p in primitives]), np.stack([p.color for p in primitives]),
+            np.array([p.source_key if p.source_key is not None else (0, 0, 0)
+                      for p in primitives], dtype=np.int64).reshape(-1, 3))
+
+    def extend_arrays(self, positions, scales, rotations, opacities, colors, source_keys):
+        k = len(opacities)
+        self._reserve(k)
+        for name, arr in (("positions", positions), ("scales", scales), ("rotations", rotations),
+                          ("opacities", opacities), ("colors", colors),
+                          ("source_keys", source_keys)):
+            self._buf[name][self._n:self._n + k] = arr
+        self._n += k
+
+    def extend_records(self, rec: dict) -> None:
+        self.extend_arrays(rec["position"], rec["scale"], rec["rotation"], rec["opacity"],
+                           rec["color"], rec["source_key"])
+
+    def primitive(self, i: int) -> GaussianPrimitive:
+        return GaussianPrimitive(
+            position=self.positions[i].copy(), scale=self.scales[i].copy(),
+            rotation=self.rotations[i].copy(), opacity=float(self.opacities[i]),
+            color=self.colors[i].copy(),
+            source_key=VoxelKey(*(int(v) for v in self.source_keys[i])))
+
+    def copy(self) -> "GaussianMap":
+        out = GaussianMap()
+        out.extend_arrays(self.positions, self.scales, self.rotations, self.opacities,
+                          self.colors, self.source_keys)
+        return out
+
+    @classmethod
+    def from_arrays(cls, positions, scales, rotations, opacities, colors,
+                    source_keys=None) -> "GaussianMap":
+        positions = np.asarray(positions, dtype=float).reshape(-1, 3)
+        n = len(positions)
+        if source_keys is None:
+            source_keys = np.zeros((n, 3), dtype=np.int64)
+        out = cls()
+        out.extend_arrays(positions, np.asarray(scales, dtype=float).reshape(n, 3),
+                          np.asarray(rotations, dtype=float).reshape(n, 4),
+                          np.asarray(opacities, dtype=float).reshape(n),
+                          np.asarray(colors, dtype=float).reshape(n, 3),
+                          np.asarray(source_keys, dtype=np.int64).reshape(n, 3))
+        return out

@@ -1,0 +1,653 @@
+"""Voxel map with a device-resident store (mirror of voxsplat/voxel_map.py).
+
+Same public names, signatures and mutation semantics as the reference
+(`/root/reference/pkg/src/voxsplat/voxel_map.py:35-399`).  The difference is
+where the cells live: `VoxelMap` owns a `VxMap` handle of libvoxgpr whose
+hash table, point arena, prediction store and lifecycle states are in HBM.
+`store_frame` (voxel_map.py:313-342) and the solves run as CUDA kernels;
+`cells`, `transitions` and `solve_log` are host views materialised from the
+device on access.  Host-only objects (`PointCloud`, `VoxelCell` built by the
+caller, `classify_voxel`, `update_voxel_variances`) keep the reference's
+pure-Python semantics because they operate on host data the caller owns.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Iterable, NamedTuple
+
+import numpy as np
+
+from . import _native as N
+from .errors import ContractViolationError, InputDomainError
+
+log = logging.getLogger(__name__)
+
+
+# ---------------------------------------------------------------------------
+# Point containers (voxel_map.py:35-105)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class ColoredPoint:
+    """A single LiDAR return: world position, RGB in [0, 1], noise variance m^2."""
+
+    position: np.ndarray
+    color: np.ndarray
+    noise_var: float
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=float).reshape(3)
+        self.color = np.asarray(self.color, dtype=float).reshape(3)
+        if not np.all(np.isfinite(self.position)):
+            raise InputDomainError("point position must be finite")
+        if np.any(self.color < 0) or np.any(self.color > 1):
+            raise InputDomainError("color components must lie in [0, 1]")
+        if self.noise_var < 0:
+            raise InputDomainError("noise_var must be nonnegative")
+
+
+@dataclass
+class PointCloud:
+    """Struct-of-arrays batch of colored points (host arrays, validated)."""
+
+    positions: np.ndarray
+    colors: np.ndarray
+    noise_var: np.ndarray
+
+    def __post_init__(self):
+        self.positions = np.asarray(self.positions, dtype=float).reshape(-1, 3)
+        self.colors = np.asarray(self.colors, dtype=float).reshape(-1, 3)
+        self.noise_var = np.asarray(self.noise_var, dtype=float).reshape(-1)
+        n = len(self.positions)
+        if len(self.colors) != n or len(self.noise_var) != n:
+            raise InputDomainError("positions, colors and noise_var must agree in length")
+        if n and not np.all(np.isfinite(self.positions)):
+            raise InputDomainError("point positions must be finite")
+        if n and (self.colors.min() < 0 or self.colors.max() > 1):
+            raise InputDomainError("color components must lie in [0, 1]")
+        if n and self.noise_var.min() < 0:
+            raise InputDomainError("noise variances must be nonnegative")
+
+    @classmethod
+    def empty(cls) -> "PointCloud":
+        return cls(np.empty((0, 3)), np.empty((0, 3)), np.empty(0))
+
+    @classmethod
+    def from_points(cls, points: Iterable[ColoredPoint]) -> "PointCloud":
+        pts = list(points)
+        if not pts:
+            return cls.empty()
+        return cls(np.stack([p.position for p in pts]), np.stack([p.color for p in pts]),
+                   np.array([p.noise_var for p in pts]))
+
+    @staticmethod
+    def concat(*clouds: "PointCloud") -> "PointCloud":
+        parts = [c for c in clouds if c is not None and len(c)]
+        if not parts:
+            return PointCloud.empty()
+        return PointCloud(np.concatenate([c.positions for c in parts]),
+                          np.concatenate([c.colors for c in parts]),
+                          np.concatenate([c.noise_var for c in parts]))
+
+    def subset(self, index) -> "PointCloud":
+        return PointCloud(self.positions[index], self.colors[index], self.noise_var[index])
+
+    def point(self, i: int) -> ColoredPoint:
+        return ColoredPoint(self.positions[i], self.colors[i], float(self.noise_var[i]))
+
+    def __len__(self) -> int:
+        return len(self.positions)
+
+
+# ---------------------------------------------------------------------------
+# Keys and states (voxel_map.py:112-149)
+# ---------------------------------------------------------------------------
+
+class VoxelKey(NamedTuple):
+    ix: int
+    iy: int
+    iz: int
+
+
+class VoxelState(IntEnum):
+    UNREADY = 0
+    READY = 1
+    ACTIVE = 2
+    CONVERGED = 3
+
+
+def voxel_keys(positions: np.ndarray, voxel_size: float) -> np.ndarray:
+    """floor(p / voxel_size) as (n, 3) int64, computed by `vx_voxel_keys`."""
+    if voxel_size <= 0:
+        raise InputDomainError("voxel_size must be positive")
+    pts = np.asarray(positions, dtype=float).reshape(-1, 3)
+    if len(pts) == 0:
+        return np.empty((0, 3), dtype=np.int64)
+    lib = N.lib()
+    import torch
+    d = N.to_device(pts)
+    out = torch.empty((len(pts), 3), dtype=torch.int64, device=d.device)
+    N.check(lib.vx_voxel_keys(N.ptr(d), len(pts), float(voxel_size), N.ptr(out), N.stream_ptr()))
+    return out.cpu().numpy()
+
+
+def voxel_key(position, voxel_size: float) -> VoxelKey:
+    """Lattice cell of a position (voxel_map.py:125-133)."""
+    if voxel_size <= 0:
+        raise InputDomainError("voxel_size must be positive")
+    p = np.asarray(position, dtype=float).reshape(3)
+    if not np.all(np.isfinite(p)):
+        raise InputDomainError("cannot hash a non-finite position")
+    k = voxel_keys(p.reshape(1, 3), voxel_size)[0]
+    return VoxelKey(int(k[0]), int(k[1]), int(k[2]))
+
+
+def voxel_bounds(key, voxel_size: float) -> np.ndarray:
+    """Axis-aligned bounds (2, 3) rows (lo, hi): lo = key * size, hi = lo + size."""
+    lo = np.array(key, dtype=float) * voxel_size
+    return np.stack([lo, lo + voxel_size])
+
+
+# ---------------------------------------------------------------------------
+# Cells, predictions, frame bookkeeping (voxel_map.py:156-221)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class VoxelPrediction:
+    key: VoxelKey
+    positions: np.ndarray
+    colors: np.ndarray
+    variances: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.positions)
+
+    @property
+    def mean_variance(self) -> float:
+        return float(self.variances.mean())
+
+
+@dataclass
+class VoxelCell:
+    key: VoxelKey
+    raw: PointCloud = field(default_factory=PointCloud.empty)
+    pseudo: PointCloud | None = None
+    state: VoxelState = VoxelState.UNREADY
+    value_axis: int | None = None
+    last_prediction: VoxelPrediction | None = None
+
+    @property
+    def solved(self) -> bool:
+        return self.last_prediction is not None
+
+    @property
+    def point_count(self) -> int:
+        return len(self.raw)
+
+    @property
+    def mean_posterior_variance(self) -> float | None:
+        if self.last_prediction is None:
+            return None
+        return self.last_prediction.mean_variance
+
+    def training_cloud(self) -> PointCloud:
+        if self.pseudo is None:
+            return self.raw
+        return PointCloud.concat(self.raw, self.pseudo)
+
+
+class FrameUpdateSet:
+    """Voxel keys touched by one frame, in first-touch order, no duplicates.
+
+    Backed by an (n, 3) int64 array; `keys` materialises VoxelKey tuples on
+    first use.  `_source` identifies the device frame list it mirrors, so
+    `densify_frame` can reuse it without re-uploading the keys.
+    """
+
+    def __init__(self, keys=None, *, array=None, source=None):
+        if array is None:
+            keys = list(keys or [])
+            array = np.array([tuple(k) for k in keys], dtype=np.int64).reshape(-1, 3)
+            self._keys = [VoxelKey(*(int(v) for v in k)) for k in keys]
+        else:
+            self._keys = None
+        self.array = np.asarray(array, dtype=np.int64).reshape(-1, 3)
+        self._source = source
+
+    @property
+    def keys(self) -> list[VoxelKey]:
+        if self._keys is None:
+            self._keys = [VoxelKey(int(a), int(b), int(c)) for a, b, c in self.array.tolist()]
+        return self._keys
+
+    def __len__(self) -> int:
+        return len(self.array)
+
+    def __iter__(self):
+        return iter(self.keys)
+
+    def __eq__(self, other):
+        if isinstance(other, FrameUpdateSet):
+            return np.array_equal(self.array, other.array)
+        return NotImplemented
+
+    def __repr__(self):
+        return f"FrameUpdateSet({len(self)} keys)"
+
+
+@dataclass
+class StateTransition:
+    frame: int
+    key: VoxelKey
+    old: VoxelState
+    new: VoxelState
+
+
+# ---------------------------------------------------------------------------
+# Pure lifecycle functions on host cells (voxel_map.py:228-261)
+# ---------------------------------------------------------------------------
+
+def classify_voxel(cell: VoxelCell, tau: int, eta: float) -> VoxelState:
+    """UNREADY/READY by point count until solved, then ACTIVE/CONVERGED by eta."""
+    if not cell.solved:
+        return VoxelState.READY if cell.point_count >= tau else VoxelState.UNREADY
+    return VoxelState.CONVERGED if cell.mean_posterior_variance <= eta else VoxelState.ACTIVE
+
+
+def update_voxel_variances(cell: VoxelCell, prediction: VoxelPrediction, tau: int,
+                           eta: float) -> VoxelCell:
+    """Fold a solve result back into a host cell and reclassify it."""
+    if prediction.key != cell.key:
+        raise ContractViolationError(
+            f"prediction for voxel {prediction.key} applied to cell {cell.key}")
+    if cell.state not in (VoxelState.READY, VoxelState.ACTIVE):
+        raise ContractViolationError(
+            f"cell {cell.key} in state {cell.state.name} cannot accept a solve")
+    cell.pseudo = PointCloud(prediction.positions, prediction.colors,
+                             np.clip(prediction.variances, 0.0, None))
+    cell.last_prediction = prediction
+    cell.state = classify_voxel(cell, tau, eta)
+    return cell
+
+
+# ---------------------------------------------------------------------------
+# The device-backed map
+# ---------------------------------------------------------------------------
+
+class _Snapshot:
+    """Host copy of the whole device store at one mutation epoch."""
+
+    def __init__(self, vmap: "VoxelMap"):
+        v = vmap._view()
+        V = int(v.num_voxels)
+        M = int(v.pred_points)
+        self.V = V
+        self.M = M
+        self.keys = N.view_tensor(v.keys, (V, 3), np.int64).cpu().numpy()
+        self.state = N.view_tensor(v.state, (V,), np.uint8).cpu().numpy()
+        self.axis = N.view_tensor(v.value_axis, (V,), np.int8).cpu().numpy()
+        self.count = N.view_tensor(v.raw_count, (V,), np.int32).cpu().numpy()
+        self.off = N.view_tensor(v.raw_offset, (V,), np.int64).cpu().numpy()
+        self.slot = N.view_tensor(v.pred_slot, (V,), np.int32).cpu().numpy()
+        self.has = N.view_tensor(v.has_pred, (V,), np.uint8).cpu().numpy()
+        top = int((self.off + self.count).max()) if V else 0
+        self.xyz = N.view_tensor(v.raw_xyz, (top, 3), np.float64).cpu().numpy()
+        self.rgb = N.view_tensor(v.raw_rgb, (top, 3), np.float64).cpu().numpy()
+        slots = int(self.slot.max()) + 1 if V and self.slot.max() >= 0 else 0
+        self.pxyz = N.view_tensor(v.pred_xyz, (slots, M, 3), np.float64).cpu().numpy()
+        self.prgb = N.view_tensor(v.pred_rgb, (slots, M, 3), np.float64).cpu().numpy()
+        self.pvar = N.view_tensor(v.pred_var, (slots, M), np.float64).cpu().numpy()
+        self.index = {tuple(k): i for i, k in enumerate(self.keys.tolist())}
+        self.sensor_var = vmap.sensor_var
+
+    def cell(self, vid: int) -> VoxelCell:
+        key = VoxelKey(*(int(x) for x in self.keys[vid]))
+        o, c = int(self.off[vid]), int(self.count[vid])
+        raw = PointCloud(self.xyz[o:o + c].copy(), self.rgb[o:o + c].copy(),
+                         np.full(c, self.sensor_var))
+        cell = VoxelCell(key=key, raw=raw, state=VoxelState(int(self.state[vid])),
+                         value_axis=None if self.axis[vid] < 0 else int(self.axis[vid]))
+        if self.has[vid]:
+            s = int(self.slot[vid])
+            pred = VoxelPrediction(key, self.pxyz[s].copy(), self.prgb[s].copy(),
+                                   self.pvar[s].copy())
+            cell.last_prediction = pred
+            cell.pseudo = PointCloud(pred.positions, pred.colors, pred.variances)
+        return cell
+
+
+class _CellsView(Mapping):
+    """`VoxelMap.cells`: dict-like, insertion (= creation) ordered, read-only."""
+
+    def __init__(self, vmap: "VoxelMap"):
+        self._m = vmap
+
+    def _snap(self) -> _Snapshot:
+        return self._m._snapshot()
+
+    def __getitem__(self, key):
+        s = self._snap()
+        vid = s.index.get(tuple(int(v) for v in key))
+        if vid is None:
+            raise KeyError(key)
+        return s.cell(vid)
+
+    def get(self, key, default=None):
+        try:
+            return self[key]
+        except KeyError:
+            return default
+
+    def __contains__(self, key):
+        try:
+            return tuple(int(v) for v in key) in self._snap().index
+        except TypeError:
+            return False
+
+    def __iter__(self):
+        s = self._snap()
+        return (VoxelKey(*(int(x) for x in k)) for k in s.keys.tolist())
+
+    def __len__(self):
+        return len(self._m)
+
+    def values(self):
+        s = self._snap()
+        return [s.cell(i) for i in range(s.V)]
+
+    def items(self):
+        s = self._snap()
+        return [(VoxelKey(*(int(x) for x in s.keys[i])), s.cell(i)) for i in range(s.V)]
+
+
+class VoxelMap:
+    """Hash map from lattice keys to cells, resident in HBM (voxel_map.py:268-399).
+
+    Single writer: every mutation is a call into libvoxgpr on the current
+    CUDA stream.  `shard_rank`/`shard_world` (B200 extension) keep only the
+    keys whose hash falls on this rank.
+    """
+
+    def __init__(self, voxel_size: float, sensor_var: float, tau: int, eta: float, *,
+                 shard_rank: int = 0, shard_world: int = 1, voxel_capacity: int = 0,
+                 point_capacity: int = 0, record_log: bool = True):
+        if voxel_size <= 0:
+            raise InputDomainError("voxel_size must be positive")
+        if sensor_var < 0:
+            raise InputDomainError("sensor_var must be nonnegative")
+        self.voxel_size = float(voxel_size)
+        self.sensor_var = float(sensor_var)
+        self.tau = int(tau)
+        self.eta = float(eta)
+        self.shard_rank, self.shard_world = int(shard_rank), int(shard_world)
+        self._capacity = (int(voxel_capacity), int(point_capacity))
+        self.record_log = record_log
+        self._handle = None
+        self._epoch = 0              # bumps on every mutation
+        self._frame_serial = 0       # bumps when the device frame list changes
+        self._snap = None
+        self._events = []            # ("t", frame, keys, old, new) / ("s", frame, keys)
+        self._transitions: list[StateTransition] = []
+        self._solve_log: list[tuple[int, VoxelKey]] = []
+        self._consumed = 0
+        self._solver = None
+        self.cells = _CellsView(self)
+
+    @classmethod
+    def from_config(cls, config, **kw) -> "VoxelMap":
+        return cls(config.voxel_size, config.sensor_var, config.tau, config.eta, **kw)
+
+    # -- native handle ------------------------------------------------------
+    def _h(self):
+        if self._handle is None:
+            lib = N.lib()
+            cfg = N.VxMapConfig()
+            cfg.voxel_size, cfg.sensor_var, cfg.tau = self.voxel_size, self.sensor_var, self.tau
+            cfg.n_s, cfg.n_r, cfg.kernel = 3, 3, 0
+            cfg.eta, cfg.kernel_lambda, cfg.jitter = self.eta, 1.0, 1e-10
+            cfg.shard_rank, cfg.shard_world = self.shard_rank, self.shard_world
+            cfg.voxel_capacity, cfg.point_capacity = self._capacity
+            h = N.vp()
+            N.check(lib.vx_map_create(C.byref(cfg), C.byref(h)))
+            self._handle = h
+            self._lib = lib
+        return self._handle
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None:
+            try:
+                self._lib.vx_map_destroy(h)
+            except Exception:
+                pass
+
+    def _view(self) -> N.VxMapView:
+        v = N.VxMapView()
+        N.check(self._lib.vx_map_view(self._h(), C.byref(v)))
+        return v
+
+    def _mutated(self):
+        self._epoch += 1
+        self._snap = None
+
+    def _snapshot(self) -> _Snapshot:
+        if self._handle is None:
+            self._h()
+        if self._snap is None or self._snap[0] != self._epoch:
+            import torch
+            torch.cuda.current_stream().synchronize()
+            self._snap = (self._epoch, _Snapshot(self))
+        return self._snap[1]
+
+    # -- accessors ----------------------------------------------------------
+    @property
+    def frame_index(self) -> int:
+        if self._handle is None:
+            return -1
+        return int(self._view().frame_index)
+
+    def __len__(self) -> int:
+        if self._handle is None:
+            return 0
+        return int(self._view().num_voxels)
+
+    def __contains__(self, key) -> bool:
+        return key in self.cells
+
+    def cell(self, key) -> VoxelCell:
+        return self.cells[key]
+
+    def cells_in_state(self, state: VoxelState) -> list[VoxelCell]:
+        s = self._snapshot()
+        return [s.cell(i) for i in np.nonzero(s.state == int(state))[0]]
+
+    def all_raw_points(self) -> PointCloud:
+        return PointCloud.concat(*(c.raw for c in self.cells.values()))
+
+    def device_view(self) -> N.VxMapView:
+        """Raw device pointers of the store (valid until the next mutation)."""
+        return self._view()
+
+    # -- event log (lazy) ---------------------------------------------------
+    def _record_transitions(self, frame, vids, old, new):
+        if not self.record_log or len(vids) == 0:
+            return
+        self._events.append(("t", frame, self._keys_of(vids), old, new))
+
+    def _record_solves(self, frame, vids, before, after):
+        if not self.record_log or len(vids) == 0:
+            return
+        self._events.append(("s", frame, self._keys_of(vids), before, after))
+
+    def _keys_of(self, vids: np.ndarray) -> np.ndarray:
+        import torch
+        v = self._view()
+        keys = N.view_tensor(v.keys, (int(v.num_voxels), 3), np.int64)
+        idx = torch.as_tensor(np.asarray(vids, dtype=np.int64), device=keys.device)
+        return keys.index_select(0, idx).cpu().numpy()
+
+    def _drain_events(self):
+        for kind, frame, keys, a, b in self._events[self._consumed:]:
+            for i, k in enumerate(keys.tolist()):
+                key = VoxelKey(*k)
+                if kind == "t":
+                    self._transitions.append(StateTransition(frame, key, VoxelState(int(a[i])),
+                                                             VoxelState(int(b[i]))))
+                else:
+                    self._solve_log.append((frame, key))
+                    # a first solve that converges passes through ACTIVE
+                    for st in range(int(a[i]) + 1, int(b[i]) + 1):
+                        self._transitions.append(StateTransition(
+                            frame, key, VoxelState(st - 1), VoxelState(st)))
+        self._consumed = len(self._events)
+
+    @property
+    def transitions(self) -> list[StateTransition]:
+        self._drain_events()
+        return self._transitions
+
+    @property
+    def solve_log(self) -> list[tuple[int, VoxelKey]]:
+        self._drain_events()
+        return self._solve_log
+
+    # -- mutation -----------------------------------------------------------
+    def store_frame(self, cloud: PointCloud) -> FrameUpdateSet:
+        """Append one frame of points to their cells (voxel_map.py:313-342)."""
+        pos = np.ascontiguousarray(cloud.positions, dtype=np.float64)
+        col = np.ascontiguousarray(cloud.colors, dtype=np.float64)
+        dpos, dcol = (N.to_device(pos), N.to_device(col)) if len(pos) else (None, None)
+        return self.store_frame_device(dpos, dcol, len(pos))
+
+    def store_frame_device(self, d_xyz, d_rgb, n: int) -> FrameUpdateSet:
+        """store_frame on device-resident (n,3) float64 tensors."""
+        h = self._h()
+        info = N.VxFrameInfo()
+        rc = self._lib.vx_map_store_frame(h, N.ptr(d_xyz), N.ptr(d_rgb), int(n), C.byref(info),
+                                          N.stream_ptr())
+        self._mutated()
+        self._frame_serial += 1
+        N.check(rc)
+        U = int(info.touched)
+        if U == 0:
+            return FrameUpdateSet(array=np.empty((0, 3), np.int64),
+                                  source=(id(self), self._frame_serial))
+        v = self._view()
+        vids = N.view_tensor(v.frame_voxels, (U,), np.int32)
+        keys_dev = N.view_tensor(v.keys, (int(v.num_voxels), 3), np.int64)
+        keys = keys_dev.index_select(0, vids.long()).cpu().numpy()
+        if self.record_log and info.ready_transitions:
+            fb = N.view_tensor(v.frame_state_before, (U,), np.uint8).cpu().numpy()
+            fa = N.view_tensor(v.frame_state_after, (U,), np.uint8).cpu().numpy()
+            ch = np.nonzero(fa != fb)[0]
+            self._events.append(("t", int(info.frame_index), keys[ch], fb[ch], fa[ch]))
+        return FrameUpdateSet(array=keys, source=(id(self), self._frame_serial))
+
+    def _configure_solver(self, config):
+        want = (int(config.n_s), int(config.n_r), float(config.kernel_lambda),
+                float(config.jitter), N.KERNELS[getattr(config, "kernel", "se")])
+        if want != self._solver:
+            N.check(self._lib.vx_map_configure_solver(self._h(), *want))
+            self._solver = want
+
+    def _select_frame(self, update_set):
+        """Make `update_set` the device frame list for the next densify."""
+        src = getattr(update_set, "_source", None)
+        if src == (id(self), self._frame_serial):
+            return
+        arr = update_set.array if isinstance(update_set, FrameUpdateSet) else \
+            np.array([tuple(k) for k in update_set], dtype=np.int64).reshape(-1, 3)
+        d = N.to_device(arr, dtype=np.int64) if len(arr) else None
+        rc = self._lib.vx_map_set_frame_keys(self._h(), N.ptr(d), len(arr), N.stream_ptr())
+        self._frame_serial += 1
+        if rc == N.VX_E_CONTRACT:
+            raise KeyError(N.last_error())
+        N.check(rc)
+        if isinstance(update_set, FrameUpdateSet):
+            update_set._source = (id(self), self._frame_serial)
+
+    def _densify(self) -> N.VxDensifyInfo:
+        info = N.VxDensifyInfo()
+        rc = self._lib.vx_map_densify(self._h(), C.byref(info), N.stream_ptr())
+        self._mutated()
+        N.check(rc)
+        return info
+
+    def apply_prediction(self, prediction: VoxelPrediction):
+        """Fold a host prediction into its device cell (voxel_map.py:344-355)."""
+        key = np.asarray(tuple(prediction.key), dtype=np.int64)
+        m = len(prediction.positions)
+        dx = N.to_device(prediction.positions)
+        dc = N.to_device(prediction.colors)
+        dv = N.to_device(prediction.variances)
+        ba = (C.c_uint8 * 2)()
+        rc = self._lib.vx_map_apply_prediction(self._h(), key.ctypes.data_as(N.c_i64p), N.ptr(dx),
+                                               N.ptr(dc), N.ptr(dv), m, ba, N.stream_ptr())
+        if rc == N.VX_E_INPUT:
+            raise KeyError(prediction.key)
+        N.check(rc)
+        self._mutated()
+        frame = self.frame_index
+        self._events.append(("s", frame, key.reshape(1, 3), np.array([ba[0]]), np.array([ba[1]])))
+        return self.cells[prediction.key]
+
+    def clear(self):
+        """Drop every voxel (B200 extension; keeps device allocations)."""
+        if self._handle is not None:
+            N.check(self._lib.vx_map_clear(self._handle, N.stream_ptr()))
+        self._mutated()
+        self._frame_serial += 1
+        self._events, self._transitions, self._solve_log, self._consumed = [], [], [], 0
+
+    # -- audits (voxel_map.py:364-399) --------------------------------------
+    def audit_transitions(self) -> list[str]:
+        issues = []
+        seq: dict = {}
+        for tr in self.transitions:
+            cur = seq.get(tr.key, int(VoxelState.UNREADY))
+            if int(tr.old) != cur or int(tr.new) != cur + 1:
+                issues.append(f"voxel {tr.key}: illegal transition "
+                              f"{tr.old.name} -> {tr.new.name} at frame {tr.frame}")
+            seq[tr.key] = int(tr.new)
+        return issues
+
+    def audit_converged_resolves(self) -> list[str]:
+        conv = {tr.key: tr.frame for tr in self.transitions if tr.new == VoxelState.CONVERGED}
+        issues = []
+        for key, fc in conv.items():
+            late = [f for f, k in self.solve_log if k == key and f > fc]
+            if late:
+                issues.append(f"voxel {key} re-solved after convergence at frames {late}")
+        return issues
+
+    def audit_hash_consistency(self) -> list[str]:
+        """Raw points whose lattice key disagrees with their cell (device check)."""
+        import torch
+        if self._handle is None:
+            return []
+        v = self._view()
+        V = int(v.num_voxels)
+        if V == 0:
+            return []
+        count = N.view_tensor(v.raw_count, (V,), np.int32).long()
+        off = N.view_tensor(v.raw_offset, (V,), np.int64)
+        top = int((off + count).max().item())
+        xyz = N.view_tensor(v.raw_xyz, (top, 3), np.float64)
+        keys = N.view_tensor(v.keys, (V, 3), np.int64)
+        owner = torch.repeat_interleave(torch.arange(V, device=keys.device), count)
+        rows = torch.repeat_interleave(off, count) + (
+            torch.arange(int(count.sum().item()), device=keys.device)
+            - torch.repeat_interleave(torch.cumsum(count, 0) - count, count))
+        pk = torch.floor(xyz[rows] / self.voxel_size).long()
+        bad = (pk != keys[owner]).any(dim=1)
+        per = torch.zeros(V, dtype=torch.int64, device=keys.device).index_add_(0, owner, bad.long())
+        idx = torch.nonzero(per).flatten().cpu().numpy()
+        kh = keys.cpu().numpy()
+        perh = per.cpu().numpy()
+        return [f"voxel {VoxelKey(*kh[i].tolist())}: {int(perh[i])} raw points hash elsewhere"
+                for i in idx]

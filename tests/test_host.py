@@ -1,0 +1,115 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared
+symbol, the package imports without a GPU, compute refuses to run on the CPU
+(no fallback), and the host-side mirrors behave like the reference."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2410_17084_b200 as vx
+from paper_2410_17084_b200 import _native as N
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _declared():
+    txt = open(os.path.join(ROOT, "include", "voxgpr.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(vx_\w+)\(", txt, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.load_library()
+    names = _declared()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(N.EXPORTED)
+    assert lib.vx_abi_version() == 1
+
+
+def test_library_built_for_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", N.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(N.NativeUnavailable):
+        vx.gpr_solve(vx.GprProblem(x=[[0, 0]], f=[1.0], noise_diag=[0.1], x_star=[[0, 0]]))
+    with pytest.raises(N.NativeUnavailable):
+        vx.VoxelMap(0.2, 1e-4, 10, 0.3).store_frame(
+            vx.PointCloud(np.zeros((1, 3)), np.zeros((1, 3)), np.zeros(1)))
+
+
+def test_error_code_mapping():
+    N.load_library()
+    with pytest.raises(vx.InputDomainError):
+        N.check(N.VX_E_INPUT)
+    with pytest.raises(vx.ContractViolationError):
+        N.check(N.VX_E_CONTRACT)
+    with pytest.raises(vx.InputDomainError):
+        N.check(N.VX_E_RANGE)
+
+
+def test_host_validation_matches_reference():
+    with pytest.raises(vx.InputDomainError):
+        vx.PointCloud(np.array([[np.nan, 0, 0]]), np.zeros((1, 3)), np.zeros(1))
+    with pytest.raises(vx.InputDomainError):
+        vx.PointCloud(np.zeros((1, 3)), np.full((1, 3), 2.0), np.zeros(1))
+    with pytest.raises(vx.InputDomainError):
+        vx.VoxelMap(0.0, 1e-4, 10, 0.3)
+    with pytest.raises(vx.InputDomainError):
+        vx.GprProblem(x=np.zeros((0, 2)), f=[], noise_diag=[], x_star=[[0, 0]])
+    with pytest.raises(ValueError):
+        vx.PipelineConfig(voxel_size=-1)
+    with pytest.raises(ValueError):
+        vx.PipelineConfig(kernel="cubic")
+
+
+def test_lifecycle_rules_on_host_cells():
+    cloud = vx.PointCloud(np.zeros((12, 3)), np.full((12, 3), 0.5), np.full(12, 0.01))
+    cell = vx.VoxelCell(key=vx.VoxelKey(1, 2, 3), raw=cloud)
+    assert vx.classify_voxel(cell, tau=10, eta=0.3) is vx.VoxelState.READY
+    cell.state = vx.VoxelState.READY
+    pred = vx.VoxelPrediction(vx.VoxelKey(1, 2, 3), np.zeros((9, 3)), np.full((9, 3), 0.5),
+                              np.full(9, 0.05))
+    vx.update_voxel_variances(cell, pred, tau=10, eta=0.3)
+    assert cell.state is vx.VoxelState.CONVERGED
+    bad = vx.VoxelPrediction(vx.VoxelKey(9, 9, 9), np.zeros((4, 3)), np.zeros((4, 3)),
+                             np.zeros(4))
+    with pytest.raises(vx.ContractViolationError):
+        vx.update_voxel_variances(cell, bad, tau=10, eta=0.3)
+
+
+def test_frame_update_set_semantics():
+    u = vx.FrameUpdateSet([(0, 0, 0), (2, 2, 2)])
+    assert len(u) == 2 and u.keys[1] == vx.VoxelKey(2, 2, 2)
+    assert list(u) == [vx.VoxelKey(0, 0, 0), vx.VoxelKey(2, 2, 2)]
+    v = vx.FrameUpdateSet(array=np.array([[0, 0, 0], [2, 2, 2]]))
+    assert u == v
+
+
+def test_gaussian_map_amortised_extend():
+    g = vx.GaussianMap()
+    prims = [vx.GaussianPrimitive(np.full(3, i), np.ones(3), [1, 0, 0, 0], 0.5, np.zeros(3),
+                                  vx.VoxelKey(i, 0, 0)) for i in range(300)]
+    for p in prims:
+        g.extend([p])
+    assert len(g) == 300
+    back = g.primitive(123)
+    np.testing.assert_array_equal(back.position, np.full(3, 123.0))
+    assert back.source_key == vx.VoxelKey(123, 0, 0)
+    h = g.copy()
+    assert len(h) == 300 and np.array_equal(h.positions, g.positions)
+
+
+def test_config_roundtrip():
+    c = vx.PipelineConfig.from_mapping({"voxel_size": "0.5", "tau": "12", "kernel": "matern52"})
+    assert c.voxel_size == 0.5 and c.tau == 12 and c.kernel == "matern52"
+    assert any(line.startswith("voxel_size=") for line in c.to_lines())

@@ -242,7 +242,7 @@ N_PROBS = (0.56, 0.29, 0.06, 0.085, 0.005)
 
 def planar_map(n_voxels=1_000_000, voxel_size=0.5, seed=0, shuffle=True,
                bins=N_BINS, probs=N_PROBS, noise=0.01, key_offset=(0, 0, 0)):
-    """(positions, colors, counts, keys) for a grid of planar voxel patches.
+    """(positions, colors, counts, keys, owner) for a grid of planar voxel patches.
 
     Voxels are the first ``n_voxels`` cells of a square ground lattice (plus
     ``key_offset``); each holds n points (n from the histogram) on a gently
@@ -273,5 +273,5 @@ def planar_map(n_voxels=1_000_000, voxel_size=0.5, seed=0, shuffle=True,
     col = rng.uniform(0.0, 1.0, (total, 3))
     if shuffle:
         perm = rng.permutation(total)
-        pos, col = pos[perm], col[perm]
-    return (np.ascontiguousarray(pos), np.ascontiguousarray(col), counts, keys)
+        pos, col, owner = pos[perm], col[perm], owner[perm]
+    return (np.ascontiguousarray(pos), np.ascontiguousarray(col), counts, keys, owner)
