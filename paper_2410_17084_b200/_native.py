@@ -214,7 +214,7 @@ class _CAI:
 
     def __init__(self, p, shape, typestr):
         self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
-                                         "data": (int(p or 0), True), "version": 2,
+                                         "data": (int(p or 0), False), "version": 2,
                                          "strides": None}
 
 

@@ -219,9 +219,11 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-// named barrier for a team of `nthreads` threads (multiple of 32)
+// named barrier for a team of `nthreads` threads (multiple of 32).  The
+// non-.aligned form: callers keep every barrier on a team-uniform path, but
+// bar.sync (== barrier.sync.aligned) would make any divergence undefined.
 __device__ __forceinline__ void team_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace vx

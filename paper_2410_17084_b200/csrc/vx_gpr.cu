@@ -455,19 +455,20 @@ __global__ void __launch_bounds__(TeamBounds<NMAX>::MAXT) gpr_team_kernel(VoxelS
                     if (i < n) t.Z[i] = w[i];
             }
             team_sync(bar, TS);
-            if (active && c > 0) {
+            const bool query = active && c > 0;
+            double mu = 0.0, var = 0.0, pos[3] = {0, 0, 0}, colr[3] = {0, 0, 0};
+            if (query) {
                 double mu0 = 0.0, mu1 = 0.0;
 #pragma unroll
                 for (int i = 0; i + 1 < NMAX; i += 2) {
                     if (i < n) mu0 = fma(w[i], t.Z[i], mu0);
                     if (i + 1 < n) mu1 = fma(w[i + 1], t.Z[i + 1], mu1);
                 }
-                const double mu = mu0 + mu1;
-                const double var = 1.0 - ss;
+                mu = mu0 + mu1;
+                var = 1.0 - ss;
                 if constexpr (VOXEL) {
-                    const double v = var < 0.0 ? 0.0 : var;     // np.clip(., 0, None)
-                    t.VAR[q] = v;
-                    double pos[3];
+                    var = var < 0.0 ? 0.0 : var;     // np.clip(., 0, None)
+                    t.VAR[q] = var;
                     const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
                     pos[axis] = xadd(mu, mean_f);
                     pos[pa_] = g0;
@@ -481,23 +482,27 @@ __global__ void __launch_bounds__(TeamBounds<NMAX>::MAXT) gpr_team_kernel(VoxelS
                     }
                     const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
                                                 : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
-                    double col0 = cs[0], col1 = cs[1], col2 = cs[2];
-                    // every read of the previous prediction precedes any write
-                    team_sync(bar, TS);
-                    const int64_t pr = int64_t(slot) * m + q;
-                    va.pred_xyz[pr * 3 + 0] = pos[0];
-                    va.pred_xyz[pr * 3 + 1] = pos[1];
-                    va.pred_xyz[pr * 3 + 2] = pos[2];
-                    va.pred_rgb[pr * 3 + 0] = col0;
-                    va.pred_rgb[pr * 3 + 1] = col1;
-                    va.pred_rgb[pr * 3 + 2] = col2;
-                    va.pred_var[pr] = v;
+                    colr[0] = cs[0];
+                    colr[1] = cs[1];
+                    colr[2] = cs[2];
                 } else {
                     pa.mu[qo + q] = mu;
                     pa.var[qo + q] = var;
                 }
-            } else if constexpr (VOXEL) {
-                team_sync(bar, TS);   // matches the barrier on the active path
+            }
+            if constexpr (VOXEL) {
+                // every read of the previous prediction precedes any write
+                team_sync(bar, TS);
+                if (query) {
+                    const int64_t pr = int64_t(slot) * m + q;
+                    va.pred_xyz[pr * 3 + 0] = pos[0];
+                    va.pred_xyz[pr * 3 + 1] = pos[1];
+                    va.pred_xyz[pr * 3 + 2] = pos[2];
+                    va.pred_rgb[pr * 3 + 0] = colr[0];
+                    va.pred_rgb[pr * 3 + 1] = colr[1];
+                    va.pred_rgb[pr * 3 + 2] = colr[2];
+                    va.pred_var[pr] = var;
+                }
             }
             team_sync(bar, TS);
         }
@@ -930,6 +935,9 @@ static int launch_team(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     if (teams < 1) teams = 1;
     if (teams > 8) teams = 8;
     if (teams * TS > TeamBounds<NMAX>::MAXT) teams = TeamBounds<NMAX>::MAXT / TS;
+    const size_t per_team = size_t(TeamLayout<NMAX>::doubles(m_max)) * sizeof(double);
+    const size_t smem_cap = 227 * 1024;
+    if (size_t(teams) * per_team > smem_cap) teams = int(smem_cap / per_team);
     if (teams < 1) {
         set_error("team of %d threads exceeds the NMAX=%d kernel bound", TS, NMAX);
         return VX_E_INPUT;
