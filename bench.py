@@ -126,6 +126,8 @@ class Clocks:
 
 def _oracle_worker(args):
     pos, col, cam, img, cfg = args
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)          # one BLAS thread per process (no oversubscription)
     from oracle import voxsplat_oracle as O
     omap = O.OracleMap(0.5, 1e-4, TAU, 0.3)
     ocam = O.OracleCamera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], cam["width"],
@@ -279,8 +281,8 @@ def run_gpu(args, rank, world, local_rank):
     top = max(stages, key=lambda k: stages[k][0])
     top_ms, top_n = stages[top]
     sol = counts[counts >= TAU]
-    bucket = {"gpr_team32": sol[sol <= 32], "gpr_team64": sol[(sol > 32) & (sol <= 64)],
-              "gpr_generic": sol[sol > 64]}
+    bucket = {"gpr_warp16": sol[sol <= 16], "gpr_warp32": sol[(sol > 16) & (sol <= 32)],
+              "gpr_warp64": sol[(sol > 32) & (sol <= 64)], "gpr_generic": sol[sol > 64]}
     if top in bucket:
         flops = float(gpr_flops(bucket[top]).sum()) * args.steps
         achieved = flops / (top_ms / 1e3) / 1e12

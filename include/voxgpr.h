@@ -304,8 +304,8 @@ int vx_init_color(const double* d_positions, const double* d_fallback, int64_t n
 int vx_fp64_peak(double* tflops, void* stream);
 
 /* CUDA-event timers around the library's stages, recorded on the launching
- * stream: 0 store_frame (hashing), 1 GPR team n<=32, 2 GPR team n<=64,
- * 3 GPR generic, 4 Gaussian init, 5 whole densify.  vx_profile(1) resets
+ * stream: 0 store_frame (hashing), 1-3 GPR warp kernels n<=16/32/64,
+ * 4 GPR generic, 5 Gaussian init, 6 whole densify, 7 PCA prepass.  vx_profile(1) resets
  * and enables; vx_profile_read fills total ms and launch counts per stage
  * and returns the number of stages. */
 int vx_profile(int enable);

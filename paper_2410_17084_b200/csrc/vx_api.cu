@@ -153,14 +153,13 @@ __global__ void k_select_axis(const double* pts, const int64_t* off, int64_t P, 
 
 // problem-mode bucketing for gpr_solve_batch
 __global__ void k_problem_buckets(const int64_t* x_off, int64_t P, int32_t* items, int* fill,
-                                  int64_t off1, int64_t off2) {
+                                  const int* base) {
     const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p >= P) return;
     const int n = int(x_off[p + 1] - x_off[p]);
     const int b = bucket_of(n);
     const int pos = atomicAdd(fill + b, 1);
-    const int64_t base = b == 0 ? 0 : (b == 1 ? off1 : off2);
-    items[base + pos] = int32_t(p);
+    items[base[b] + pos] = int32_t(p);
 }
 __global__ void k_problem_count(const int64_t* x_off, int64_t P, int* counts) {
     const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -363,15 +362,22 @@ int vx_gpr_solve_batch(const VxGprBatch* b, void* stream) {
     const unsigned g = unsigned((P + 255) / 256);
     k_problem_count<<<g, 256, 0, s>>>(b->d_x_off, P, cnt);
     count_launch();
-    VX_CUDA(cudaMemcpyAsync(sc.host, cnt, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    VX_CUDA(cudaMemcpyAsync(sc.host, cnt, NUM_BUCKETS * sizeof(int), cudaMemcpyDeviceToHost, s));
     VX_CUDA(cudaStreamSynchronize(s));
-    const int c0 = sc.host[0], c1 = sc.host[1], c2 = sc.host[2];
-    k_problem_buckets<<<g, 256, 0, s>>>(b->d_x_off, P, sc.a.as<int32_t>(), cnt + 4, c0, c0 + c1);
+    int counts[NUM_BUCKETS];
+    int64_t offs[NUM_BUCKETS];
+    int64_t acc = 0;
+    for (int k = 0; k < NUM_BUCKETS; ++k) {
+        counts[k] = sc.host[k];
+        offs[k] = acc;
+        sc.host[8 + k] = int(acc);
+        acc += counts[k];
+    }
+    VX_CUDA(cudaMemcpyAsync(cnt + 8, sc.host + 8, NUM_BUCKETS * sizeof(int), cudaMemcpyHostToDevice, s));
+    k_problem_buckets<<<g, 256, 0, s>>>(b->d_x_off, P, sc.a.as<int32_t>(), cnt + 4, cnt + 8);
     count_launch();
     VX_CHECK_LAUNCH();
-    const int counts[3] = {c0, c1, c2};
-    const int64_t offs[3] = {0, c0, c0 + c1};
-    for (int k = 2; k >= 0; --k) {
+    for (int k = NUM_BUCKETS - 1; k >= 0; --k) {
         if (counts[k] == 0) continue;
         VX_TRY(launch_problem_solve(*b, sc.a.as<int32_t>() + offs[k], counts[k], b->max_n, b->max_m,
                                     sc.c, s, k));

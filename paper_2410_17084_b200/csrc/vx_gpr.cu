@@ -4,18 +4,22 @@
 // gpr_solve, densify_frame's per-voxel body) and voxel_map.py:242-261 /
 // 344-355 (apply_prediction's fold-back and reclassification).
 //
-// Two kernel families, chosen per training-set size n (size buckets):
+// Stages, chosen per training-set size n (size buckets):
 //
-//  * team kernel (n <= 64): a "team" of 32*ceil((m+1)/32) threads owns one
-//    voxel at a time; several teams per CTA, each synchronised by its own
-//    named barrier.  The team builds A = K + diag(noise) in shared memory,
-//    factorises it (one warp, rows in registers, warp shuffles, for n <= 32;
-//    team-parallel left-looking in shared memory for n <= 64), then every
-//    thread owns one right-hand side column of [f | K*] and runs a
-//    left-looking forward substitution with the column held in registers:
+//  * PCA prepass (thread per voxel): centroid, 3x3 covariance, Jacobi eigen,
+//    value axis + degeneracy test (gpr.py:57-78) and the pairwise mean of the
+//    targets (gpr.py:291).  Decouples the serial per-voxel work from the
+//    solve kernels and lets degenerate voxels drop out before bucketing.
+//  * warp kernel (n <= 16 / 32 / 64): ONE WARP per voxel, no CTA barriers.
+//    The warp builds A = K + diag(noise) column-major in its shared-memory
+//    slice, factorises it left-looking (lanes = rows, dot products against
+//    the broadcast pivot row, one __syncwarp per column), then every lane
+//    owns one right-hand side column of [f | K*] per pass (ceil((m+1)/32)
+//    passes) and runs a right-looking forward substitution with the column
+//    in registers and L columns read as 16-byte pairs:
 //        w = L^-1 k*_c,  sigma^2_c = 1 - |w|^2,  mu_c = w . (L^-1 f).
 //    K* is never materialised: for the SE kernel on the voxel's regular grid
-//    k*(x_i, g) = exp(-lam dx^2) exp(-lam dy^2) is separable, so the team
+//    k*(x_i, g) = exp(-lam dx^2) exp(-lam dy^2) is separable, so the warp
 //    tabulates 2 * n * (n_s n_r) exponentials instead of n * (n_s n_r)^2.
 //  * generic kernel (any n): one CTA per voxel, A/L (column-major) and W in a
 //    per-CTA global workspace (L2-resident), left-looking Cholesky and a
@@ -58,37 +62,106 @@ struct ProblemArgs {
 };
 
 // ---------------------------------------------------------------------------
-// shared-memory carve-up of one team (small kernel)
+// PCA prepass: one thread per candidate voxel
 // ---------------------------------------------------------------------------
-template <int NMAX>
-struct TeamLayout {
-    static constexpr int LD = NMAX + 1;           // odd stride: conflict-free rows
-    int mmax;                                     // max query count
-    __host__ __device__ static int doubles(int mmax) {
-        return NMAX * 2 /*X*/ + NMAX /*F*/ + NMAX /*NZ*/ + NMAX /*Z*/ +
-               NMAX * LD /*L (also 3-D staging)*/ + 2 * NMAX * MAX_MM /*EA,EB*/ +
-               mmax /*VAR*/ + 8 /*misc*/;
+__device__ __forceinline__ const double* train_point(const VoxelSolveArgs& a, int r, int cnt,
+                                                     int64_t off, int slot) {
+    return r < cnt ? a.raw_xyz + (off + r) * 3
+                   : a.pred_xyz + (int64_t(slot) * a.M + (r - cnt)) * 3;
+}
+
+__global__ void __launch_bounds__(128) k_pca_prepass(VoxelSolveArgs a, int S, long long* buckets) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const int vid = a.cand_voxel[s];
+    const int n = a.cand_n[s];
+    const int cnt = a.raw_count[vid];
+    const int64_t off = a.raw_offset[vid];
+    const int slot = a.pred_slot[vid];
+    int ax = -1;
+    if (n >= 3) {
+        // pts.mean(axis=0): sequential accumulation (NumPy reduces axis 0 row by row)
+        double mx = 0.0, my = 0.0, mz = 0.0;
+        for (int r = 0; r < n; ++r) {
+            const double* p = train_point(a, r, cnt, off, slot);
+            mx = xadd(mx, p[0]);
+            my = xadd(my, p[1]);
+            mz = xadd(mz, p[2]);
+        }
+        mx = xdiv(mx, double(n));
+        my = xdiv(my, double(n));
+        mz = xdiv(mz, double(n));
+        double c[6] = {0, 0, 0, 0, 0, 0};
+        for (int r = 0; r < n; ++r) {
+            const double* p = train_point(a, r, cnt, off, slot);
+            const double dx = xsub(p[0], mx), dy = xsub(p[1], my), dz = xsub(p[2], mz);
+            c[0] = fma(dx, dx, c[0]);
+            c[1] = fma(dx, dy, c[1]);
+            c[2] = fma(dx, dz, c[2]);
+            c[3] = fma(dy, dy, c[3]);
+            c[4] = fma(dy, dz, c[4]);
+            c[5] = fma(dz, dz, c[5]);
+        }
+        for (int k = 0; k < 6; ++k) c[k] /= double(n);
+        double ev[3], v0[3];
+        eig3_sym(c, ev, v0, nullptr);
+        if (!(ev[2] <= 1e-18 || ev[1] <= 1e-9 * ev[2])) {     // gpr.py:73-74
+            const double w0 = fabs(v0[0]), w1 = fabs(v0[1]), w2 = fabs(v0[2]);
+            ax = 2;                                              // ties prefer z, then y
+            double best = w2;
+            if (w1 > best) { ax = 1; best = w1; }
+            if (w0 > best) ax = 0;
+        }
+    }
+    a.cand_axis[s] = int8_t(ax);
+    if (ax < 0) {
+        a.cand_status[s] = VX_ST_DEGENERATE;
+        const uint8_t st = a.state[vid];
+        a.cand_before[s] = st;
+        a.cand_after[s] = st;
+        return;
+    }
+    const double sum = np_pairwise_sum(
+        [&](int i) { return train_point(a, i, cnt, off, slot)[ax]; }, n);
+    a.cand_meanf[s] = xdiv(sum, double(n));                    // f.mean() (gpr.py:291)
+    atomicAdd(reinterpret_cast<unsigned long long*>(buckets + bucket_of(n)), 1ull);
+}
+
+__global__ void k_bucket_items(const int32_t* cand_n, const int8_t* cand_axis, int S, int32_t* items,
+                               const long long* base, long long* fill) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S || cand_axis[s] < 0) return;
+    const int b = bucket_of(cand_n[s]);
+    const long long pos = atomicAdd(reinterpret_cast<unsigned long long*>(fill + b), 1ull);
+    items[base[b] + pos] = int32_t(s);
+}
+
+// ---------------------------------------------------------------------------
+// warp-per-voxel kernel (n <= NMAX, NMAX in {16, 32, 64})
+// ---------------------------------------------------------------------------
+// per-warp shared-memory slice (doubles), LD = NMAX (even: 16-byte columns)
+struct WarpLayout {
+    int X, F, NZ, L, INV, EA, EB, MU, VAR, COL, BI, total;
+    __host__ __device__ WarpLayout(int NMAX, int mm, int m, bool voxel) {
+        int o = 0;
+        X = o; o += 2 * NMAX;
+        F = o; o += NMAX;
+        NZ = o; o += NMAX;            // noise, later z = L^-1 f
+        L = o; o += NMAX * NMAX;
+        INV = o; o += NMAX;
+        EA = o; EB = o;
+        MU = VAR = COL = BI = o;
+        if (voxel) {
+            EA = o; o += NMAX * mm;
+            EB = o; o += NMAX * mm;
+            MU = o; o += m;
+            VAR = o; o += m;
+            COL = o; o += 3 * m;
+            BI = o; o += (m + 1) / 2;  // int32 pairs
+        }
+        total = (o + 1) & ~1;
     }
 };
-
-struct TeamPtrs {
-    double *X, *F, *NZ, *Z, *L, *EA, *EB, *VAR, *misc;
-};
-
-template <int NMAX>
-__device__ __forceinline__ TeamPtrs carve(double* base, int mmax) {
-    TeamPtrs p;
-    p.X = base;
-    p.F = p.X + NMAX * 2;
-    p.NZ = p.F + NMAX;
-    p.Z = p.NZ + NMAX;
-    p.L = p.Z + NMAX;
-    p.EA = p.L + NMAX * TeamLayout<NMAX>::LD;
-    p.EB = p.EA + NMAX * MAX_MM;
-    p.VAR = p.EB + NMAX * MAX_MM;
-    p.misc = p.VAR + mmax;
-    return p;
-}
 
 // triangular index -> (i, j), j <= i
 __device__ __forceinline__ void tri_decode(int idx, int* i, int* j) {
@@ -99,125 +172,30 @@ __device__ __forceinline__ void tri_decode(int idx, int* i, int* j) {
     *j = idx - r * (r + 1) / 2;
 }
 
-// build A = K + diag(noise) (+ jitter on the retry) into row-major L
-template <int LD>
-__device__ void team_build_A(const TeamPtrs& t, int n, double lam, int kind, double jit,
-                             int tid, int TS) {
-    const int tot = n * (n + 1) / 2;
-    for (int idx = tid; idx < tot; idx += TS) {
-        int i, j;
-        tri_decode(idx, &i, &j);
-        double v;
-        if (i == j) {
-            // K_ii = exp(-lam * 0) = 1 exactly, then + noise (gpr.py:185),
-            // then + jitter on the retry (gpr.py:189)
-            v = xadd(1.0, t.NZ[i]);
-            if (jit != 0.0) v = xadd(v, jit);
-        } else {
-            double d2 = dist2_exact(t.X[2 * i], t.X[2 * i + 1], t.X[2 * j], t.X[2 * j + 1]);
-            v = kernel_value(kind, lam, d2);
-        }
-        t.L[i * LD + j] = v;
-    }
-}
-
-// Cholesky of the n x n (n <= 32) lower triangle in t.L by one warp; row i in
-// lane i's registers.  Fails (returns false) on a pivot that is not > 0,
-// which is dpotrf's rule (pivot <= 0 or NaN).
-template <int LD>
-__device__ bool warp_cholesky32(double* L, int n, int lane) {
-    double a[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) a[j] = (lane < n && j <= lane) ? L[lane * LD + j] : 0.0;
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        if (k < n && ok) {
-            double akk = __shfl_sync(FULL, a[k], k);
-            if (!(akk > 0.0)) {
-                ok = false;
-            } else {
-                double lkk = sqrt(akk);
-                if (lane == k) a[k] = lkk;
-                else if (lane > k) a[k] = a[k] / lkk;
-                double lik = a[k];
-#pragma unroll
-                for (int j = k + 1; j < 32; ++j) {
-                    if (j < n) {
-                        double ljk = __shfl_sync(FULL, a[k], j);
-                        if (lane >= j) a[j] = fma(-lik, ljk, a[j]);
-                    }
-                }
-            }
-        }
-    }
-    if (ok && lane < n) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j <= lane) L[lane * LD + j] = a[j];
-    }
-    __syncwarp();
-    return ok;
-}
-
-// team-parallel left-looking Cholesky in shared memory (row-major, odd LD):
-// column j: s_i = A_ij - sum_{k<j} L_ik L_jk for i >= j; L_jj = sqrt(s_j);
-// L_ij = s_i / L_jj.  Returns false on a non-positive pivot (uniform).
-template <int LD>
-__device__ bool team_cholesky(double* L, int n, int tid, int TS, int bar, double* flag) {
-    for (int j = 0; j < n; ++j) {
-        for (int i = j + tid; i < n; i += TS) {
-            const double* Li = L + i * LD;
-            const double* Lj = L + j * LD;
-            double s0 = Li[j], s1 = 0.0;
-            int k = 0;
-            for (; k + 1 < j; k += 2) {
-                s0 = fma(-Li[k], Lj[k], s0);
-                s1 = fma(-Li[k + 1], Lj[k + 1], s1);
-            }
-            if (k < j) s0 = fma(-Li[k], Lj[k], s0);
-            L[i * LD + j] = s0 + s1;
-        }
-        team_sync(bar, TS);
-        double d = L[j * LD + j];
-        if (!(d > 0.0)) return false;
-        double ljj = sqrt(d);
-        for (int i = j + 1 + tid; i < n; i += TS) L[i * LD + j] = L[i * LD + j] / ljj;
-        team_sync(bar, TS);
-        if (tid == 0) L[j * LD + j] = ljj;
-        // the diagonal write is read only after the next barrier
-    }
-    team_sync(bar, TS);
-    return true;
-}
-
-// ---------------------------------------------------------------------------
-// the team kernel
-// ---------------------------------------------------------------------------
-template <int NMAX>
-struct TeamBounds {
-    static constexpr int MAXT = NMAX <= 32 ? 384 : 256;
-};
-
 template <int NMAX, bool VOXEL>
-__global__ void __launch_bounds__(TeamBounds<NMAX>::MAXT) gpr_team_kernel(VoxelSolveArgs va, ProblemArgs pa,
-                                                       int TS, int teams, int mmax) {
-    extern __shared__ double smem[];
-    constexpr int LD = TeamLayout<NMAX>::LD;
-    const int team = threadIdx.x / TS;
-    const int tid = threadIdx.x % TS;
-    const int bar = 1 + team;
+__global__ void __launch_bounds__(128) gpr_warp_kernel(VoxelSolveArgs va, ProblemArgs pa, int mmax,
+                                                       int mm) {
+    extern __shared__ __align__(16) double smem[];
+    constexpr int LD = NMAX;
+    constexpr int RPL = NMAX > 32 ? 2 : 1;          // Cholesky rows per lane
     const int lane = threadIdx.x & 31;
-    const int twarp = tid >> 5;
-    TeamPtrs t = carve<NMAX>(smem + size_t(team) * TeamLayout<NMAX>::doubles(mmax), mmax);
-    int* imisc = reinterpret_cast<int*>(t.misc + 4);
-
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const WarpLayout lay(NMAX, mm, mmax, VOXEL);
+    double* base = smem + size_t(wib) * lay.total;
+    double* X = base + lay.X;
+    double* F = base + lay.F;
+    double* NZ = base + lay.NZ;
+    double* L = base + lay.L;
+    double* INV = base + lay.INV;
     const int num_items = VOXEL ? va.num_items : pa.num_items;
-    for (int it = blockIdx.x * teams + team; it < num_items; it += gridDim.x * teams) {
-        int n, m, s = 0, vid = 0, cnt = 0, slot = 0, axis = 2, mm = 1;
+
+    for (int it = blockIdx.x * wpb + wib; it < num_items; it += gridDim.x * wpb) {
+        int n, m, s, vid = 0, cnt = 0, slot = 0, axis = 2;
         int64_t off = 0, xo = 0, qo = 0;
         double lam, jitter, mean_f = 0.0;
         int kind;
+        double lo0 = 0, lo1 = 0, sp0 = 0, sp1 = 0;
         if constexpr (VOXEL) {
             s = va.items[it];
             vid = va.cand_voxel[s];
@@ -226,108 +204,39 @@ __global__ void __launch_bounds__(TeamBounds<NMAX>::MAXT) gpr_team_kernel(VoxelS
             off = va.raw_offset[vid];
             slot = va.pred_slot[vid];
             m = va.M;
-            mm = va.n_s * va.n_r;
             lam = va.lam;
             jitter = va.jitter;
             kind = va.kernel;
-            // ---- stage raw ∪ pseudo (voxel_map.py:196-200) as 3-D points in L
-            double* P3 = t.L;
-            const bool hp = va.has_pred[vid] != 0;
-            for (int r = tid; r < n; r += TS) {
-                const double* src;
-                double nz;
-                if (r < cnt) {
-                    src = va.raw_xyz + (off + r) * 3;
-                    nz = va.sensor_var;
-                } else {
-                    int64_t pr = int64_t(slot) * m + (r - cnt);
-                    src = va.pred_xyz + pr * 3;
-                    nz = va.pred_var[pr];
-                }
-                P3[r * 3 + 0] = src[0];
-                P3[r * 3 + 1] = src[1];
-                P3[r * 3 + 2] = src[2];
-                t.NZ[r] = nz;
-            }
-            (void)hp;
-            team_sync(bar, TS);
-            // ---- value axis by PCA (gpr.py:57-78), warp 0 of the team
-            if (twarp == 0) {
-                double mx = 0.0, my = 0.0, mz = 0.0;
-                if (lane == 0) {
-                    // pts.mean(axis=0): sequential accumulation, then / n
-                    for (int r = 0; r < n; ++r) {
-                        mx = xadd(mx, P3[r * 3]);
-                        my = xadd(my, P3[r * 3 + 1]);
-                        mz = xadd(mz, P3[r * 3 + 2]);
-                    }
-                    mx = xdiv(mx, double(n));
-                    my = xdiv(my, double(n));
-                    mz = xdiv(mz, double(n));
-                }
-                mx = __shfl_sync(FULL, mx, 0);
-                my = __shfl_sync(FULL, my, 0);
-                mz = __shfl_sync(FULL, mz, 0);
-                double c[6] = {0, 0, 0, 0, 0, 0};
-                for (int r = lane; r < n; r += 32) {
-                    double dx = xsub(P3[r * 3], mx), dy = xsub(P3[r * 3 + 1], my),
-                           dz = xsub(P3[r * 3 + 2], mz);
-                    c[0] = fma(dx, dx, c[0]);
-                    c[1] = fma(dx, dy, c[1]);
-                    c[2] = fma(dx, dz, c[2]);
-                    c[3] = fma(dy, dy, c[3]);
-                    c[4] = fma(dy, dz, c[4]);
-                    c[5] = fma(dz, dz, c[5]);
-                }
-#pragma unroll
-                for (int k = 0; k < 6; ++k)
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(FULL, c[k], o);
-                if (lane == 0) {
-                    int ax = -1;
-                    if (n >= 3) {
-                        for (int k = 0; k < 6; ++k) c[k] /= double(n);
-                        double ev[3], v0[3];
-                        eig3_sym(c, ev, v0, nullptr);
-                        if (!(ev[2] <= 1e-18 || ev[1] <= 1e-9 * ev[2])) {
-                            double w0 = fabs(v0[0]), w1 = fabs(v0[1]), w2 = fabs(v0[2]);
-                            // argmax over (z, y, x): ties prefer z, then y
-                            ax = 2;
-                            double best = w2;
-                            if (w1 > best) { ax = 1; best = w1; }
-                            if (w0 > best) { ax = 0; }
-                        }
-                    }
-                    imisc[0] = ax;
-                }
-            }
-            team_sync(bar, TS);
-            axis = imisc[0];
-            if (axis < 0) {
-                if (tid == 0) {
-                    va.cand_status[s] = VX_ST_DEGENERATE;
-                    uint8_t st = va.state[vid];
-                    va.cand_before[s] = st;
-                    va.cand_after[s] = st;
-                }
-                team_sync(bar, TS);
-                continue;
-            }
+            axis = va.cand_axis[s];
+            mean_f = va.cand_meanf[s];
             const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
-            for (int r = tid; r < n; r += TS) {
-                t.X[2 * r] = P3[r * 3 + pa_];
-                t.X[2 * r + 1] = P3[r * 3 + pb_];
-                t.F[r] = P3[r * 3 + axis];
+            // ---- stage raw ∪ pseudo (voxel_map.py:196-200), split by axis
+            for (int r = lane; r < n; r += 32) {
+                const double* p = train_point(va, r, cnt, off, slot);
+                X[2 * r] = p[pa_];
+                X[2 * r + 1] = p[pb_];
+                F[r] = xsub(p[axis], mean_f);
+                NZ[r] = r < cnt ? va.sensor_var : va.pred_var[int64_t(slot) * m + (r - cnt)];
             }
-            team_sync(bar, TS);
-            if (tid == 0) {
-                const double* F = t.F;
-                double sum = np_pairwise_sum([F](int i) { return F[i]; }, n);
-                t.misc[0] = xdiv(sum, double(n));     // f.mean() (gpr.py:291)
+            // ---- voxel grid (gpr.py:104-120, 262-266): lo + ((i + 0.5) * (hi - lo)) / m
+            lo0 = xmul(double(va.keys[int64_t(vid) * 3 + pa_]), va.voxel_size);
+            lo1 = xmul(double(va.keys[int64_t(vid) * 3 + pb_]), va.voxel_size);
+            sp0 = xsub(xadd(lo0, va.voxel_size), lo0);
+            sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
+            __syncwarp();
+            if (kind == VX_KERNEL_SE) {
+                double* EA = base + lay.EA;
+                double* EB = base + lay.EB;
+                for (int e = lane; e < 2 * n * mm; e += 32) {
+                    const int which = e >= n * mm;
+                    const int rem = e - which * n * mm;
+                    const int i = rem / mm, r = rem - i * mm;
+                    const double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
+                    const double g = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
+                    const double d = xsub(X[2 * i + which], g);
+                    (which ? EB : EA)[i * mm + r] = exp(xmul(-lam, xmul(d, d)));
+                }
             }
-            team_sync(bar, TS);
-            mean_f = t.misc[0];
-            for (int r = tid; r < n; r += TS) t.F[r] = xsub(t.F[r], mean_f);
         } else {
             s = pa.items[it];
             xo = pa.x_off[s];
@@ -337,89 +246,105 @@ __global__ void __launch_bounds__(TeamBounds<NMAX>::MAXT) gpr_team_kernel(VoxelS
             lam = pa.lam[s];
             jitter = pa.jitter;
             kind = pa.kernel;
-            for (int r = tid; r < n; r += TS) {
-                t.X[2 * r] = pa.x[(xo + r) * 2];
-                t.X[2 * r + 1] = pa.x[(xo + r) * 2 + 1];
-                t.F[r] = pa.f[xo + r];
-                t.NZ[r] = pa.noise[xo + r];
+            for (int r = lane; r < n; r += 32) {
+                X[2 * r] = pa.x[(xo + r) * 2];
+                X[2 * r + 1] = pa.x[(xo + r) * 2 + 1];
+                F[r] = pa.f[xo + r];
+                NZ[r] = pa.noise[xo + r];
             }
         }
-        team_sync(bar, TS);
+        __syncwarp();
 
-        // ---- A = K + diag(noise); Cholesky; one jitter retry (gpr.py:184-194)
+        // ---- A = K + diag(noise), Cholesky, one jitter retry (gpr.py:184-194)
         bool ok = false;
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
-            team_build_A<LD>(t, n, lam, kind, attempt ? jitter : 0.0, tid, TS);
-            team_sync(bar, TS);
-            if constexpr (NMAX <= 32) {
-                if (twarp == 0) {
-                    bool r = warp_cholesky32<LD>(t.L, n, lane);
-                    if (lane == 0) imisc[1] = r ? 1 : 0;
+            const double jit = attempt ? jitter : 0.0;
+            const int tot = n * (n + 1) / 2;
+            for (int e = lane; e < tot; e += 32) {
+                int i, j;
+                tri_decode(e, &i, &j);
+                double v;
+                if (i == j) {
+                    v = xadd(1.0, NZ[i]);          // K_ii = exp(-lam*0) = 1, + noise
+                    if (jit != 0.0) v = xadd(v, jit);
+                } else {
+                    v = kernel_value(kind, lam,
+                                     dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
                 }
-                team_sync(bar, TS);
-                ok = imisc[1] != 0;
-            } else {
-                ok = team_cholesky<LD>(t.L, n, tid, TS, bar, t.misc);
+                L[j * LD + i] = v;                 // column-major lower triangle
             }
-            team_sync(bar, TS);
+            __syncwarp();
+            ok = true;
+            for (int j = 0; j < n; ++j) {
+                double sv[RPL];
+#pragma unroll
+                for (int rr = 0; rr < RPL; ++rr) {
+                    const int i = j + lane + 32 * rr;
+                    double s0 = 0.0, s1 = 0.0;
+                    if (i < n) {
+                        s0 = L[j * LD + i];
+                        int k = 0;
+                        for (; k + 1 < j; k += 2) {
+                            s0 = fma(-L[k * LD + i], L[k * LD + j], s0);
+                            s1 = fma(-L[(k + 1) * LD + i], L[(k + 1) * LD + j], s1);
+                        }
+                        if (k < j) s0 = fma(-L[k * LD + i], L[k * LD + j], s0);
+                    }
+                    sv[rr] = s0 + s1;
+                }
+                const double d = __shfl_sync(FULL, sv[0], 0);   // pivot row j is lane 0
+                if (!(d > 0.0)) {                                 // dpotrf: pivot <= 0 or NaN
+                    ok = false;
+                    break;
+                }
+                const double ljj = sqrt(d);
+                const double inv = 1.0 / ljj;                     // dpotf2 scales by 1/ajj
+#pragma unroll
+                for (int rr = 0; rr < RPL; ++rr) {
+                    const int i = j + lane + 32 * rr;
+                    if (i < n) L[j * LD + i] = (i == j) ? ljj : sv[rr] * inv;
+                }
+                if (lane == 0) INV[j] = inv;
+                __syncwarp();
+            }
+            __syncwarp();
         }
         if (!ok) {
-            if (tid == 0) {
+            if (lane == 0) {
                 if constexpr (VOXEL) {
                     va.cand_status[s] = VX_ST_CHOL_FAIL;
-                    uint8_t st = va.state[vid];
+                    const uint8_t st = va.state[vid];
                     va.cand_before[s] = st;
                     va.cand_after[s] = st;
                 } else {
                     pa.status[s] = VX_ST_CHOL_FAIL;
                 }
             }
-            team_sync(bar, TS);
+            __syncwarp();
             continue;
         }
 
-        // ---- voxel grid (gpr.py:104-120, 262-266) and separable SE tables
-        double lo0 = 0, lo1 = 0, sp0 = 0, sp1 = 0;
-        const bool sep = VOXEL && kind == VX_KERNEL_SE;
-        if constexpr (VOXEL) {
-            const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
-            lo0 = xmul(double(va.keys[vid * 3 + pa_]), va.voxel_size);
-            lo1 = xmul(double(va.keys[vid * 3 + pb_]), va.voxel_size);
-            sp0 = xsub(xadd(lo0, va.voxel_size), lo0);    // hi - lo
-            sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
-            if (sep) {
-                for (int e = tid; e < 2 * n * mm; e += TS) {
-                    int which = e / (n * mm);
-                    int rem = e - which * n * mm;
-                    int i = rem / mm, r = rem - i * mm;
-                    double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
-                    double g = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
-                    double d = xsub(t.X[2 * i + which], g);
-                    (which ? t.EB : t.EA)[i * mm + r] = exp(xmul(-lam, xmul(d, d)));
-                }
-            }
-        }
-        team_sync(bar, TS);
-
-        // ---- forward substitution: thread owns column c of [f | K*]
+        // ---- forward substitution, lane = one column of [f | K*] per pass
         const int ncols = m + 1;
-        const int passes = (ncols + TS - 1) / TS;
+        const int passes = (ncols + 31) >> 5;
+        const double* EA = base + lay.EA;
+        const double* EB = base + lay.EB;
         for (int pass = 0; pass < passes; ++pass) {
-            const int c = pass * TS + tid;
+            const int c = pass * 32 + lane;
             const bool active = c < ncols;
             const int q = c - 1;
             double g0 = 0, g1 = 0;
             int ri = 0, si = 0;
             if (active && c > 0) {
                 if constexpr (VOXEL) {
-                    const int nr2 = va.n_r * va.n_r;
-                    const int sr = q / (va.n_s * nr2);
-                    const int rem = q - sr * va.n_s * nr2;
+                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+                    const int sr = q / (ns * nr2);
+                    const int rem = q - sr * ns * nr2;
                     const int sc = rem / nr2;
                     const int rem2 = rem - sc * nr2;
-                    const int fr = rem2 / va.n_r, fc = rem2 - fr * va.n_r;
-                    ri = sr * va.n_r + fr;
-                    si = sc * va.n_r + fc;
+                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                    ri = sr * nr + fr;
+                    si = sc * nr + fc;
                     g0 = xadd(lo0, xdiv(xmul(double(ri) + 0.5, sp0), double(mm)));
                     g1 = xadd(lo1, xdiv(xmul(double(si) + 0.5, sp1), double(mm)));
                 } else {
@@ -427,102 +352,123 @@ __global__ void __launch_bounds__(TeamBounds<NMAX>::MAXT) gpr_team_kernel(VoxelS
                     g1 = pa.xs[(qo + q) * 2 + 1];
                 }
             }
-            double w[NMAX];
+            double b[NMAX];
+#pragma unroll
+            for (int i = 0; i < NMAX; ++i) {
+                double r = 0.0;
+                if (i < n) {
+                    if (c == 0) r = F[i];
+                    else if (!active) r = 0.0;
+                    else if (VOXEL && kind == VX_KERNEL_SE) r = EA[i * mm + ri] * EB[i * mm + si];
+                    else r = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], g0, g1));
+                }
+                b[i] = r;
+            }
             double ss = 0.0;
 #pragma unroll
             for (int i = 0; i < NMAX; ++i) {
                 if (i < n) {
-                    double rhs;
-                    if (c == 0) rhs = t.F[i];
-                    else if (!active) rhs = 0.0;
-                    else if (sep) rhs = t.EA[i * mm + ri] * t.EB[i * mm + si];
-                    else rhs = kernel_value(kind, lam, dist2_exact(t.X[2 * i], t.X[2 * i + 1], g0, g1));
-                    const double* Li = t.L + i * LD;
-                    double b0 = rhs, b1 = 0.0;
+                    const double w = b[i] * INV[i];
+                    ss = fma(w, w, ss);
+                    const double* Lc = L + i * LD;            // column i: L(r, i) at Lc[r]
 #pragma unroll
-                    for (int j = 0; j + 1 < i; j += 2) {
-                        b0 = fma(-Li[j], w[j], b0);
-                        b1 = fma(-Li[j + 1], w[j + 1], b1);
+                    for (int r = (i + 1) & ~1; r < NMAX; r += 2) {
+                        if (r < n) {
+                            const double2 l2 = *reinterpret_cast<const double2*>(Lc + r);
+                            b[r] = fma(-l2.x, w, b[r]);
+                            if (r + 1 < NMAX) b[r + 1] = fma(-l2.y, w, b[r + 1]);
+                        }
                     }
-                    if (i & 1) b0 = fma(-Li[i - 1], w[i - 1], b0);
-                    w[i] = (b0 + b1) / Li[i];
-                    ss = fma(w[i], w[i], ss);
+                    b[i] = w;                                  // (r == i above touched a dead value)
                 }
             }
-            if (c == 0) {
+            if (pass == 0) {
+                if (lane == 0) {
 #pragma unroll
-                for (int i = 0; i < NMAX; ++i)
-                    if (i < n) t.Z[i] = w[i];
+                    for (int i = 0; i < NMAX; ++i)
+                        if (i < n) NZ[i] = b[i];              // z = L^-1 f
+                }
+                __syncwarp();
             }
-            team_sync(bar, TS);
-            const bool query = active && c > 0;
-            double mu = 0.0, var = 0.0, pos[3] = {0, 0, 0}, colr[3] = {0, 0, 0};
-            if (query) {
+            if (active && c > 0) {
                 double mu0 = 0.0, mu1 = 0.0;
 #pragma unroll
-                for (int i = 0; i + 1 < NMAX; i += 2) {
-                    if (i < n) mu0 = fma(w[i], t.Z[i], mu0);
-                    if (i + 1 < n) mu1 = fma(w[i + 1], t.Z[i + 1], mu1);
+                for (int i = 0; i < NMAX; i += 2) {
+                    if (i < n) mu0 = fma(b[i], NZ[i], mu0);
+                    if (i + 1 < n) mu1 = fma(b[i + 1], NZ[i + 1], mu1);
                 }
-                mu = mu0 + mu1;
-                var = 1.0 - ss;
+                const double mu = mu0 + mu1;
+                const double var = 1.0 - ss;
                 if constexpr (VOXEL) {
-                    var = var < 0.0 ? 0.0 : var;     // np.clip(., 0, None)
-                    t.VAR[q] = var;
-                    const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
-                    pos[axis] = xadd(mu, mean_f);
-                    pos[pa_] = g0;
-                    pos[pb_] = g1;
+                    base[lay.MU + q] = xadd(mu, mean_f);
+                    base[lay.VAR + q] = var < 0.0 ? 0.0 : var;      // np.clip(., 0, None)
                     // nearest training point in the parameter plane (gpr.py:304-305)
                     double best = INFINITY;
                     int bi = 0;
                     for (int i = 0; i < n; ++i) {
-                        double d2 = dist2_exact(g0, g1, t.X[2 * i], t.X[2 * i + 1]);
+                        const double d2 = dist2_exact(g0, g1, X[2 * i], X[2 * i + 1]);
                         if (d2 < best) { best = d2; bi = i; }
                     }
-                    const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
-                                                : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
-                    colr[0] = cs[0];
-                    colr[1] = cs[1];
-                    colr[2] = cs[2];
+                    reinterpret_cast<int*>(base + lay.BI)[q] = bi;
                 } else {
                     pa.mu[qo + q] = mu;
                     pa.var[qo + q] = var;
                 }
             }
-            if constexpr (VOXEL) {
-                // every read of the previous prediction precedes any write
-                team_sync(bar, TS);
-                if (query) {
-                    const int64_t pr = int64_t(slot) * m + q;
-                    va.pred_xyz[pr * 3 + 0] = pos[0];
-                    va.pred_xyz[pr * 3 + 1] = pos[1];
-                    va.pred_xyz[pr * 3 + 2] = pos[2];
-                    va.pred_rgb[pr * 3 + 0] = colr[0];
-                    va.pred_rgb[pr * 3 + 1] = colr[1];
-                    va.pred_rgb[pr * 3 + 2] = colr[2];
-                    va.pred_var[pr] = var;
-                }
-            }
-            team_sync(bar, TS);
         }
-        if (tid == 0) {
-            if constexpr (VOXEL) {
-                const double* V = t.VAR;
-                double mv = xdiv(np_pairwise_sum([V](int i) { return V[i]; }, m), double(m));
-                uint8_t before = va.state[vid];
-                uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
+        if constexpr (VOXEL) {
+            __syncwarp();
+            double* COL = base + lay.COL;
+            const int* BI = reinterpret_cast<const int*>(base + lay.BI);
+            // read phase: colours may come from the previous prediction of this voxel
+            for (int q = lane; q < m; q += 32) {
+                const int bi = BI[q];
+                const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
+                                            : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
+                COL[q * 3] = cs[0];
+                COL[q * 3 + 1] = cs[1];
+                COL[q * 3 + 2] = cs[2];
+            }
+            __syncwarp();
+            const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
+            double* oxyz = va.pred_xyz + int64_t(slot) * m * 3;
+            double* orgb = va.pred_rgb + int64_t(slot) * m * 3;
+            double* ovar = va.pred_var + int64_t(slot) * m;
+            const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+            for (int q = lane; q < m; q += 32) {
+                const int sr = q / (ns * nr2);
+                const int rem = q - sr * ns * nr2;
+                const int sc = rem / nr2;
+                const int rem2 = rem - sc * nr2;
+                const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                double pos[3];
+                pos[axis] = base[lay.MU + q];
+                pos[pa_] = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
+                pos[pb_] = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
+                oxyz[q * 3] = pos[0];
+                oxyz[q * 3 + 1] = pos[1];
+                oxyz[q * 3 + 2] = pos[2];
+                orgb[q * 3] = COL[q * 3];
+                orgb[q * 3 + 1] = COL[q * 3 + 1];
+                orgb[q * 3 + 2] = COL[q * 3 + 2];
+                ovar[q] = base[lay.VAR + q];
+            }
+            if (lane == 0) {
+                const double* V = base + lay.VAR;
+                const double mv = xdiv(np_pairwise_sum([V](int i) { return V[i]; }, m), double(m));
+                const uint8_t before = va.state[vid];
+                const uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
                 va.state[vid] = after;
                 va.value_axis[vid] = int8_t(axis);
                 va.has_pred[vid] = 1;
                 va.cand_status[s] = VX_ST_OK;
                 va.cand_before[s] = before;
                 va.cand_after[s] = after;
-            } else {
-                pa.status[s] = VX_ST_OK;
             }
+        } else {
+            if (lane == 0) pa.status[s] = VX_ST_OK;
         }
-        team_sync(bar, TS);
+        __syncwarp();
     }
 }
 
@@ -560,9 +506,6 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 template <bool VOXEL>
 __global__ void __launch_bounds__(GB) gpr_generic_kernel(VoxelSolveArgs va, ProblemArgs pa,
                                                          GenericWork gw) {
-    __shared__ double red[32];
-    __shared__ int ishared[4];
-    __shared__ double dshared[4];
     const int tid = threadIdx.x;
     double* ws = gw.base + int64_t(blockIdx.x) * gw.per_cta;
     const int NM = gw.nmax, MM = gw.mmax;
@@ -592,90 +535,16 @@ __global__ void __launch_bounds__(GB) gpr_generic_kernel(VoxelSolveArgs va, Prob
             lam = va.lam;
             jitter = va.jitter;
             kind = va.kernel;
-            for (int r = tid; r < n; r += GB) {
-                const double* src;
-                double nz;
-                if (r < cnt) {
-                    src = va.raw_xyz + (off + r) * 3;
-                    nz = va.sensor_var;
-                } else {
-                    int64_t pr = int64_t(slot) * m + (r - cnt);
-                    src = va.pred_xyz + pr * 3;
-                    nz = va.pred_var[pr];
-                }
-                P3[r * 3 + 0] = src[0];
-                P3[r * 3 + 1] = src[1];
-                P3[r * 3 + 2] = src[2];
-                NZ[r] = nz;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                double mx = 0, my = 0, mz = 0;
-                for (int r = 0; r < n; ++r) {
-                    mx = xadd(mx, P3[r * 3]);
-                    my = xadd(my, P3[r * 3 + 1]);
-                    mz = xadd(mz, P3[r * 3 + 2]);
-                }
-                dshared[0] = xdiv(mx, double(n));
-                dshared[1] = xdiv(my, double(n));
-                dshared[2] = xdiv(mz, double(n));
-            }
-            __syncthreads();
-            const double mx = dshared[0], my = dshared[1], mz = dshared[2];
-            double c[6] = {0, 0, 0, 0, 0, 0};
-            for (int r = tid; r < n; r += GB) {
-                double dx = xsub(P3[r * 3], mx), dy = xsub(P3[r * 3 + 1], my),
-                       dz = xsub(P3[r * 3 + 2], mz);
-                c[0] = fma(dx, dx, c[0]);
-                c[1] = fma(dx, dy, c[1]);
-                c[2] = fma(dx, dz, c[2]);
-                c[3] = fma(dy, dy, c[3]);
-                c[4] = fma(dy, dz, c[4]);
-                c[5] = fma(dz, dz, c[5]);
-            }
-            for (int k = 0; k < 6; ++k) c[k] = block_sum(c[k], red);
-            if (tid == 0) {
-                int ax = -1;
-                if (n >= 3) {
-                    for (int k = 0; k < 6; ++k) c[k] /= double(n);
-                    double ev[3], v0[3];
-                    eig3_sym(c, ev, v0, nullptr);
-                    if (!(ev[2] <= 1e-18 || ev[1] <= 1e-9 * ev[2])) {
-                        double w0 = fabs(v0[0]), w1 = fabs(v0[1]), w2 = fabs(v0[2]);
-                        ax = 2;
-                        double best = w2;
-                        if (w1 > best) { ax = 1; best = w1; }
-                        if (w0 > best) { ax = 0; }
-                    }
-                }
-                ishared[0] = ax;
-            }
-            __syncthreads();
-            axis = ishared[0];
-            if (axis < 0) {
-                if (tid == 0) {
-                    va.cand_status[s] = VX_ST_DEGENERATE;
-                    uint8_t st = va.state[vid];
-                    va.cand_before[s] = st;
-                    va.cand_after[s] = st;
-                }
-                __syncthreads();
-                continue;
-            }
+            axis = va.cand_axis[s];
+            mean_f = va.cand_meanf[s];
             const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
             for (int r = tid; r < n; r += GB) {
-                X[2 * r] = P3[r * 3 + pa_];
-                X[2 * r + 1] = P3[r * 3 + pb_];
-                F[r] = P3[r * 3 + axis];
+                const double* p = train_point(va, r, cnt, off, slot);
+                X[2 * r] = p[pa_];
+                X[2 * r + 1] = p[pb_];
+                F[r] = xsub(p[axis], mean_f);
+                NZ[r] = r < cnt ? va.sensor_var : va.pred_var[int64_t(slot) * m + (r - cnt)];
             }
-            __syncthreads();
-            if (tid == 0) {
-                double sum = np_pairwise_sum([F](int i) { return F[i]; }, n);
-                dshared[3] = xdiv(sum, double(n));
-            }
-            __syncthreads();
-            mean_f = dshared[3];
-            for (int r = tid; r < n; r += GB) F[r] = xsub(F[r], mean_f);
         } else {
             s = pa.items[it];
             xo = pa.x_off[s];
@@ -920,36 +789,21 @@ __global__ void __launch_bounds__(GB) gpr_generic_kernel(VoxelSolveArgs va, Prob
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
-// one pass over the m+1 right-hand sides whenever m < 1024 (voxel mode
-// relies on it: every read of the previous prediction precedes every write)
-static int team_threads_for(int m) {
-    int ts = ((m + 1 + 31) / 32) * 32;
-    return ts > 1024 ? 1024 : ts;
-}
-
 template <int NMAX, bool VOXEL>
-static int launch_team(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int m_max,
-                       cudaStream_t s) {
-    const int TS = team_threads_for(m_max);
-    int teams = 384 / TS;
-    if (teams < 1) teams = 1;
-    if (teams > 8) teams = 8;
-    if (teams * TS > TeamBounds<NMAX>::MAXT) teams = TeamBounds<NMAX>::MAXT / TS;
-    const size_t per_team = size_t(TeamLayout<NMAX>::doubles(m_max)) * sizeof(double);
-    const size_t smem_cap = 227 * 1024;
-    if (size_t(teams) * per_team > smem_cap) teams = int(smem_cap / per_team);
-    if (teams < 1) {
-        set_error("team of %d threads exceeds the NMAX=%d kernel bound", TS, NMAX);
-        return VX_E_INPUT;
-    }
-    const size_t smem = size_t(teams) * TeamLayout<NMAX>::doubles(m_max) * sizeof(double);
-    auto kfn = gpr_team_kernel<NMAX, VOXEL>;
+static int launch_warp(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int m_max,
+                       int mm, cudaStream_t s) {
+    if (num_items <= 0) return VX_OK;
+    const WarpLayout lay(NMAX, mm, m_max, VOXEL);
+    const size_t per_warp = size_t(lay.total) * sizeof(double);
+    int wpb = 4;
+    while (wpb > 1 && per_warp * wpb > size_t(100) * 1024) --wpb;
+    const size_t smem = per_warp * wpb;
+    auto kfn = gpr_warp_kernel<NMAX, VOXEL>;
     VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int blocks = (num_items + teams - 1) / teams;
-    const int cap = sm_count() * 8;
+    int blocks = (num_items + wpb - 1) / wpb;
+    const int cap = sm_count() * 16;
     if (blocks > cap) blocks = cap;
-    if (blocks < 1) return VX_OK;
-    kfn<<<blocks, teams * TS, smem, s>>>(va, pa, TS, teams, m_max);
+    kfn<<<blocks, 32 * wpb, smem, s>>>(va, pa, m_max, mm);
     count_launch();
     VX_CHECK_LAUNCH();
     return VX_OK;
@@ -959,8 +813,9 @@ template <bool VOXEL>
 static int launch_generic(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int n_max,
                           int m_max, DevBuf& work, cudaStream_t s) {
     if (num_items <= 0) return VX_OK;
-    const int64_t per = int64_t(n_max > m_max ? n_max : m_max) * 3 + int64_t(n_max) * 2 + 2 * int64_t(n_max) + m_max +
-                        int64_t(n_max) * n_max + int64_t(n_max) * (m_max + 1) + 16;
+    const int64_t per = int64_t(n_max > m_max ? n_max : m_max) * 3 + int64_t(n_max) * 2 +
+                        2 * int64_t(n_max) + m_max + int64_t(n_max) * n_max +
+                        int64_t(n_max) * (m_max + 1) + 16;
     int blocks = num_items;
     const int cap = sm_count() * 4;
     if (blocks > cap) blocks = cap;
@@ -975,18 +830,38 @@ static int launch_generic(const VoxelSolveArgs& va, const ProblemArgs& pa, int n
     return VX_OK;
 }
 
+int launch_pca_prepass(const VoxelSolveArgs& a, int S, long long* bucket_counts, cudaStream_t s) {
+    if (S <= 0) return VX_OK;
+    k_pca_prepass<<<(S + 127) / 128, 128, 0, s>>>(a, S, bucket_counts);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
+int launch_bucket_items(const VoxelSolveArgs& a, int S, int32_t* items, const long long* base,
+                        long long* fill, cudaStream_t s) {
+    if (S <= 0) return VX_OK;
+    k_bucket_items<<<(S + 255) / 256, 256, 0, s>>>(a.cand_n, a.cand_axis, S, items, base, fill);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
 int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStream_t s,
                        int bucket) {
     ProblemArgs none{};
     if (a.num_items <= 0) return VX_OK;
-    if (a.n_s * a.n_r > MAX_MM) {
-        set_error("n_s * n_r = %d exceeds %d", a.n_s * a.n_r, MAX_MM);
+    const int mm = a.n_s * a.n_r;
+    if (mm > MAX_MM) {
+        set_error("n_s * n_r = %d exceeds %d", mm, MAX_MM);
         return VX_E_INPUT;
     }
-    if (bucket == 0) return launch_team<32, true>(a, none, a.num_items, a.M, s);
-    if (bucket == 1 && team_threads_for(a.M) <= TeamBounds<64>::MAXT)
-        return launch_team<64, true>(a, none, a.num_items, a.M, s);
-    return launch_generic<true>(a, none, a.num_items, max_n, a.M, work, s);
+    switch (bucket) {
+        case 0: return launch_warp<16, true>(a, none, a.num_items, a.M, mm, s);
+        case 1: return launch_warp<32, true>(a, none, a.num_items, a.M, mm, s);
+        case 2: return launch_warp<64, true>(a, none, a.num_items, a.M, mm, s);
+        default: return launch_generic<true>(a, none, a.num_items, max_n, a.M, work, s);
+    }
 }
 
 int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t count, int max_n,
@@ -996,10 +871,10 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
                    b.d_lam, b.jitter, b.kernel, b.d_mu, b.d_var, b.d_full, b.d_full_off,
                    b.d_status};
     if (count <= 0) return VX_OK;
-    if (b.d_full == nullptr && team_threads_for(max_m) <= TeamBounds<32>::MAXT) {
-        if (bucket == 0) return launch_team<32, false>(none, pa, count, max_m, s);
-        if (bucket == 1 && team_threads_for(max_m) <= TeamBounds<64>::MAXT)
-            return launch_team<64, false>(none, pa, count, max_m, s);
+    if (b.d_full == nullptr) {
+        if (bucket == 0) return launch_warp<16, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 1) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 2) return launch_warp<64, false>(none, pa, count, max_m, 1, s);
     }
     return launch_generic<false>(none, pa, count, max_n, max_m, work, s);
 }

@@ -37,7 +37,7 @@ inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Optional CUDA-event timers around the library's stages (vx_profile_*).
-enum ProfStage { P_HASH = 0, P_GPR_SMALL, P_GPR_MEDIUM, P_GPR_GENERIC, P_SPLAT, P_DENSIFY, P_COUNT };
+enum ProfStage { P_HASH = 0, P_GPR_B0, P_GPR_B1, P_GPR_B2, P_GPR_GENERIC, P_SPLAT, P_DENSIFY, P_PCA, P_COUNT };
 void prof_begin(int stage, cudaStream_t s);
 void prof_end(int stage, cudaStream_t s);
 
@@ -74,6 +74,8 @@ struct VoxelSolveArgs {
     uint8_t* cand_status;      // (S)
     uint8_t* cand_before;      // (S)
     uint8_t* cand_after;       // (S)
+    int8_t* cand_axis;         // (S) value axis from the PCA prepass, -1 degenerate
+    double* cand_meanf;        // (S) pairwise mean of the targets
     // store
     const int64_t* keys;       // (V,3)
     uint8_t* state;
@@ -98,10 +100,15 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
 int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t count,
                          int max_n, int max_m, DevBuf& work, cudaStream_t s, int bucket);
 
-// bucket boundaries for the training-set size n
-constexpr int BUCKET_SMALL = 32;
-constexpr int BUCKET_MEDIUM = 64;
-__host__ __device__ inline int bucket_of(int n) { return n <= BUCKET_SMALL ? 0 : (n <= BUCKET_MEDIUM ? 1 : 2); }
+// bucket boundaries for the training-set size n: warp kernels for n <= 16,
+// 32, 64 and the generic kernel beyond
+constexpr int NUM_BUCKETS = 4;
+__host__ __device__ inline int bucket_of(int n) {
+    return n <= 16 ? 0 : (n <= 32 ? 1 : (n <= 64 ? 2 : 3));
+}
+int launch_pca_prepass(const VoxelSolveArgs& a, int S, long long* bucket_counts, cudaStream_t s);
+int launch_bucket_items(const VoxelSolveArgs& a, int S, int32_t* items, const long long* base,
+                        long long* fill, cudaStream_t s);
 
 // ---------------------------------------------------------------- splat init
 int launch_gaussians(const double* pred_xyz, const double* pred_rgb, const double* pred_var,

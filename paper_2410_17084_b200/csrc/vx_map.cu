@@ -54,7 +54,7 @@ struct VxMap {
     int64_t frame_touched = 0;
     // densify
     vx::DevBuf cflag, cscan, cand_voxel, cand_n, cand_status, cand_before, cand_after, items,
-        okflag, okscan, solved_vids;
+        okflag, okscan, solved_vids, cand_axis, cand_meanf;
     int64_t solve_candidates = 0, solved = 0;
     // counters (device) + pinned mirror
     vx::DevBuf counters;
@@ -77,8 +77,9 @@ enum {
     C_S,              // densify candidates
     C_MAXN,
     C_NEWSLOTS,
-    C_B0, C_B1, C_B2, // bucket counts
-    C_F0, C_F1, C_F2, // bucket fill cursors
+    C_B0, C_B1, C_B2, C_B3,   // bucket counts
+    C_F0, C_F1, C_F2, C_F3,   // bucket fill cursors
+    C_O0, C_O1, C_O2, C_O3,   // bucket bases
     C_OK, C_DEGEN, C_CHOL, C_FIRST, C_CONV,
     C_COUNT
 };
@@ -341,21 +342,10 @@ __global__ void k_dens_list(const int32_t* frame_vids, const int32_t* cflag, con
     cand_n[s] = n;
     cand_status[s] = 255;
     atomicMax(reinterpret_cast<unsigned long long*>(ctr + C_MAXN), (unsigned long long)n);
-    atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_B0 + bucket_of(n)), 1ull);
     if (pred_slot[vid] < 0) {
         const long long k = atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_NEWSLOTS), 1ull);
         pred_slot[vid] = int32_t(slot_base + k);
     }
-}
-
-__global__ void k_bucket_fill(const int32_t* cand_n, int64_t S, int32_t* items, int64_t off1,
-                              int64_t off2, long long* ctr) {
-    const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (s >= S) return;
-    const int b = bucket_of(cand_n[s]);
-    const long long pos = atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_F0 + b), 1ull);
-    const int64_t base = b == 0 ? 0 : (b == 1 ? off1 : off2);
-    items[base + pos] = int32_t(s);
 }
 
 __global__ void k_dens_finish(const uint8_t* status, const uint8_t* before, const uint8_t* after,
@@ -707,15 +697,11 @@ static int map_densify_impl(VxMap* m, VxDensifyInfo* info, cudaStream_t s) {
     VX_TRY(read_counters(m, s));
     const int64_t newslots = m->host_counters[C_NEWSLOTS];
     const int max_n = int(m->host_counters[C_MAXN]);
-    const int64_t b0 = m->host_counters[C_B0], b1 = m->host_counters[C_B1],
-                  b2 = m->host_counters[C_B2];
     di.max_train = max_n;
     VX_TRY(ensure_slots(m, m->num_slots + newslots, s));
     m->num_slots += newslots;
-    k_bucket_fill<<<nblk(S), 256, 0, s>>>(m->cand_n.as<int32_t>(), S, m->items.as<int32_t>(), b0,
-                                          b0 + b1, ctr(m));
-    count_launch();
-    VX_CHECK_LAUNCH();
+    VX_TRY(m->cand_axis.reserve(S, s));
+    VX_TRY(m->cand_meanf.reserve(S * 8, s));
 
     VoxelSolveArgs a{};
     a.cand_voxel = m->cand_voxel.as<int32_t>();
@@ -723,6 +709,8 @@ static int map_densify_impl(VxMap* m, VxDensifyInfo* info, cudaStream_t s) {
     a.cand_status = m->cand_status.as<uint8_t>();
     a.cand_before = m->cand_before.as<uint8_t>();
     a.cand_after = m->cand_after.as<uint8_t>();
+    a.cand_axis = m->cand_axis.as<int8_t>();
+    a.cand_meanf = m->cand_meanf.as<double>();
     a.keys = m->keys3.as<int64_t>();
     a.state = m->state.as<uint8_t>();
     a.value_axis = m->axis.as<int8_t>();
@@ -744,16 +732,31 @@ static int map_densify_impl(VxMap* m, VxDensifyInfo* info, cudaStream_t s) {
     a.n_r = m->cfg.n_r;
     a.kernel = m->cfg.kernel;
     a.M = m->M;
+
+    // PCA prepass: value axis, degeneracy, target mean; bucket counts
+    prof_begin(P_PCA, s);
+    VX_TRY(launch_pca_prepass(a, int(S), ctr(m) + C_B0, s));
+    prof_end(P_PCA, s);
+    VX_TRY(read_counters(m, s));
+    int64_t counts[NUM_BUCKETS], offs[NUM_BUCKETS];
+    int64_t acc = 0;
+    for (int b = 0; b < NUM_BUCKETS; ++b) {
+        counts[b] = m->host_counters[C_B0 + b];
+        offs[b] = acc;
+        acc += counts[b];
+        m->host_counters[C_O0 + b] = offs[b];
+    }
+    VX_CUDA(cudaMemcpyAsync(ctr(m) + C_O0, m->host_counters + C_O0, NUM_BUCKETS * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, s));
+    VX_TRY(launch_bucket_items(a, int(S), m->items.as<int32_t>(), ctr(m) + C_O0, ctr(m) + C_F0, s));
     // largest buckets first so their tails overlap the small ones
-    const int64_t counts[3] = {b0, b1, b2};
-    const int64_t offs[3] = {0, b0, b0 + b1};
-    for (int b = 2; b >= 0; --b) {
+    for (int b = NUM_BUCKETS - 1; b >= 0; --b) {
         if (counts[b] == 0) continue;
         a.items = m->items.as<int32_t>() + offs[b];
         a.num_items = int32_t(counts[b]);
-        prof_begin(P_GPR_SMALL + b, s);
+        prof_begin(P_GPR_B0 + b, s);
         VX_TRY(launch_voxel_solve(a, max_n, m->gpr_work, s, b));
-        prof_end(P_GPR_SMALL + b, s);
+        prof_end(P_GPR_B0 + b, s);
     }
     k_dens_finish<<<nblk(S), 256, 0, s>>>(m->cand_status.as<uint8_t>(), m->cand_before.as<uint8_t>(),
                                           m->cand_after.as<uint8_t>(), S, m->okflag.as<int32_t>(),
@@ -858,7 +861,7 @@ void map_delete(VxMap* m) {
                       &m->tseg, &m->tnew, &m->tnewscan, &m->tneed, &m->tneedscan, &m->tbase,
                       &m->treloc, &m->frame_vids, &m->fb, &m->fa, &m->cflag, &m->cscan,
                       &m->cand_voxel, &m->cand_n, &m->cand_status, &m->cand_before, &m->cand_after,
-                      &m->items, &m->okflag, &m->okscan, &m->solved_vids, &m->counters, &m->scan_tmp,
+                      &m->items, &m->okflag, &m->okscan, &m->solved_vids, &m->cand_axis, &m->cand_meanf, &m->counters, &m->scan_tmp,
                       &m->sort_tmp, &m->gpr_work, &m->stage};
     for (DevBuf* b : bufs) b->release();
     if (m->host_counters) cudaFreeHost(m->host_counters);
