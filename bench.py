@@ -282,7 +282,8 @@ def run_gpu(args, rank, world, local_rank):
     top_ms, top_n = stages[top]
     sol = counts[counts >= TAU]
     bucket = {"gpr_warp16": sol[sol <= 16], "gpr_warp32": sol[(sol > 16) & (sol <= 32)],
-              "gpr_warp64": sol[(sol > 32) & (sol <= 64)], "gpr_generic": sol[sol > 64]}
+              "gpr_warp64": sol[(sol > 32) & (sol <= 64)],
+              "gpr_cta128": sol[(sol > 64) & (sol <= 128)], "gpr_cta_large": sol[sol > 128]}
     if top in bucket:
         flops = float(gpr_flops(bucket[top]).sum()) * args.steps
         achieved = flops / (top_ms / 1e3) / 1e12

@@ -305,7 +305,8 @@ int vx_fp64_peak(double* tflops, void* stream);
 
 /* CUDA-event timers around the library's stages, recorded on the launching
  * stream: 0 store_frame (hashing), 1-3 GPR warp kernels n<=16/32/64,
- * 4 GPR generic, 5 Gaussian init, 6 whole densify, 7 PCA prepass.  vx_profile(1) resets
+ * 4-5 GPR CTA kernels n<=128 / n>128, 6 Gaussian init, 7 whole densify,
+ * 8 PCA prepass.  vx_profile(1) resets
  * and enables; vx_profile_read fills total ms and launch counts per stage
  * and returns the number of stages. */
 int vx_profile(int enable);

@@ -258,8 +258,8 @@ def splat_struct(n_s, n_r, weight_floor, scale_floor, opacity, rotation="identit
     return s
 
 
-PROFILE_STAGES = ("hash", "gpr_warp16", "gpr_warp32", "gpr_warp64", "gpr_generic", "splat",
-                  "densify", "pca")
+PROFILE_STAGES = ("hash", "gpr_warp16", "gpr_warp32", "gpr_warp64", "gpr_cta128", "gpr_cta_large",
+                  "splat", "densify", "pca")
 
 
 def profile(enable: bool) -> None:

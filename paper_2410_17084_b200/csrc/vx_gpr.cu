@@ -787,6 +787,455 @@ __global__ void __launch_bounds__(GB) gpr_generic_kernel(VoxelSolveArgs va, Prob
 }
 
 // ---------------------------------------------------------------------------
+// blocked CTA kernel (n > 64): one voxel per CTA of CT threads
+// ---------------------------------------------------------------------------
+// Buffers live in one workspace that is the CTA's dynamic shared memory when
+// it fits, else a per-CTA slice of global memory (L2-resident):
+//   Lp   packed column-major lower triangle; column j starts at row (j & ~1)
+//        and is padded to an even length so L(r, j) pairs with even r are
+//        16-byte aligned (element (i, j) at off[j] + i - (j & ~1))
+//   W    row-major n x WLD right-hand-side block of the current column pass
+// Cholesky: left-looking by panels of P = 8 columns.  Each thread owns rows
+//   and updates P accumulators per previous column k with one load of L(i,k)
+//   and four 16-byte loads of L(J,k) (8 FMAs : 5 loads); the P x P diagonal
+//   block is then factorised redundantly in every thread's registers (same
+//   values -> same pivot decision, no extra barrier) and applied to the
+//   thread's rows.  dpotrf's failure rule, one jitter retry.
+// Forward substitution: a thread owns one column of [f | K*]; rows go in
+//   chunks of CH = 16 held in registers; each previous row j contributes
+//   acc(R) -= L(R, j) w_j with 8 paired 16-byte loads per 16 FMAs.
+constexpr int CT = 96;
+constexpr int PNL = 8;
+constexpr int CH = 16;
+
+struct CtaLayout {
+    int64_t X, F, NZ, INV, EA, EB, MU, VAR, COL, BI, OFF, Lp, W, total;
+    int n_pad, wld;
+    __host__ __device__ CtaLayout(int n, int mm, int m, bool voxel) {
+        n_pad = (n + 1) & ~1;
+        const int cols = m + 1;
+        wld = cols < CT ? cols : CT;
+        int64_t o = 0;
+        X = o; o += 2 * n_pad;
+        F = o; o += n_pad;
+        NZ = o; o += n_pad;            // noise, later z = L^-1 f
+        INV = o; o += n_pad;
+        EA = EB = MU = VAR = COL = BI = o;
+        if (voxel) {
+            EA = o; o += int64_t(n_pad) * mm;
+            EB = o; o += int64_t(n_pad) * mm;
+            MU = o; o += m + (m & 1);
+            VAR = o; o += m + (m & 1);
+            COL = o; o += 3 * m + (m & 1);
+            BI = o; o += (m + 1) / 2 + ((m + 1) / 2 & 1);
+        }
+        OFF = o; o += (n_pad + 2) / 2 + 2;    // int32 column offsets (as doubles)
+        o = (o + 1) & ~int64_t(1);
+        Lp = o;
+        const int64_t hp = n_pad / 2;
+        o += 2 * (hp * n_pad - hp * (hp - 1)) + 2 * PNL + 4;
+        o = (o + 1) & ~int64_t(1);
+        W = o; o += int64_t(n_pad + CH) * wld;
+        total = (o + 1) & ~int64_t(1);
+    }
+};
+
+template <bool VOXEL>
+__global__ void __launch_bounds__(CT) gpr_cta_kernel(VoxelSolveArgs va, ProblemArgs pa, int nmax,
+                                                     int mmax, int mm, double* gwork, int64_t per_cta) {
+    extern __shared__ __align__(16) double smem[];
+    const int tid = threadIdx.x;
+    const CtaLayout lay(nmax, mm, mmax, VOXEL);
+    double* base = gwork ? gwork + int64_t(blockIdx.x) * per_cta : smem;
+    double* X = base + lay.X;
+    double* F = base + lay.F;
+    double* NZ = base + lay.NZ;
+    double* INV = base + lay.INV;
+    int* OFF = reinterpret_cast<int*>(base + lay.OFF);
+    double* Lp = base + lay.Lp;
+    double* W = base + lay.W;
+    const int num_items = VOXEL ? va.num_items : pa.num_items;
+
+    for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
+        int n, m, s, vid = 0, cnt = 0, slot = 0, axis = 2;
+        int64_t off = 0, xo = 0, qo = 0;
+        double lam, jitter, mean_f = 0.0;
+        int kind;
+        double lo0 = 0, lo1 = 0, sp0 = 0, sp1 = 0;
+        if constexpr (VOXEL) {
+            s = va.items[it];
+            vid = va.cand_voxel[s];
+            n = va.cand_n[s];
+            cnt = va.raw_count[vid];
+            off = va.raw_offset[vid];
+            slot = va.pred_slot[vid];
+            m = va.M;
+            lam = va.lam;
+            jitter = va.jitter;
+            kind = va.kernel;
+            axis = va.cand_axis[s];
+            mean_f = va.cand_meanf[s];
+            const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
+            for (int r = tid; r < n; r += CT) {
+                const double* p = train_point(va, r, cnt, off, slot);
+                X[2 * r] = p[pa_];
+                X[2 * r + 1] = p[pb_];
+                F[r] = xsub(p[axis], mean_f);
+                NZ[r] = r < cnt ? va.sensor_var : va.pred_var[int64_t(slot) * m + (r - cnt)];
+            }
+            lo0 = xmul(double(va.keys[int64_t(vid) * 3 + pa_]), va.voxel_size);
+            lo1 = xmul(double(va.keys[int64_t(vid) * 3 + pb_]), va.voxel_size);
+            sp0 = xsub(xadd(lo0, va.voxel_size), lo0);
+            sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
+            __syncthreads();
+            if (kind == VX_KERNEL_SE) {
+                double* EA = base + lay.EA;
+                double* EB = base + lay.EB;
+                for (int e = tid; e < 2 * n * mm; e += CT) {
+                    const int which = e >= n * mm;
+                    const int rem = e - which * n * mm;
+                    const int i = rem / mm, r = rem - i * mm;
+                    const double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
+                    const double g = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
+                    const double d = xsub(X[2 * i + which], g);
+                    (which ? EB : EA)[i * mm + r] = exp(xmul(-lam, xmul(d, d)));
+                }
+            }
+        } else {
+            s = pa.items[it];
+            xo = pa.x_off[s];
+            qo = pa.q_off[s];
+            n = int(pa.x_off[s + 1] - xo);
+            m = int(pa.q_off[s + 1] - qo);
+            lam = pa.lam[s];
+            jitter = pa.jitter;
+            kind = pa.kernel;
+            for (int r = tid; r < n; r += CT) {
+                X[2 * r] = pa.x[(xo + r) * 2];
+                X[2 * r + 1] = pa.x[(xo + r) * 2 + 1];
+                F[r] = pa.f[xo + r];
+                NZ[r] = pa.noise[xo + r];
+            }
+        }
+        const int n_pad = (n + 1) & ~1;
+        // packed column offsets: columns 2u and 2u+1 both hold n_pad - 2u rows
+        for (int j = tid; j <= n; j += CT) {
+            const int u = j >> 1;
+            int o = 2 * (u * n_pad - u * (u - 1));
+            if (j & 1) o += n_pad - 2 * u;
+            OFF[j] = o;
+        }
+        __syncthreads();
+        auto Lat = [&](int i, int j) -> double& { return Lp[OFF[j] + i - (j & ~1)]; };
+
+        // ---- A = K + diag(noise), panel Cholesky, one jitter retry
+        bool ok = false;
+        for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+            const double jit = attempt ? jitter : 0.0;
+            for (int j = 0; j < n; ++j) {
+                for (int i = j + tid; i < n; i += CT) {
+                    double v;
+                    if (i == j) {
+                        v = xadd(1.0, NZ[i]);
+                        if (jit != 0.0) v = xadd(v, jit);
+                    } else {
+                        v = kernel_value(kind, lam,
+                                         dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
+                    }
+                    Lat(i, j) = v;
+                }
+            }
+            __syncthreads();
+            ok = true;
+            for (int j0 = 0; j0 < n; j0 += PNL) {
+                const int pw = min(PNL, n - j0);
+                // phase 1: A(i, J) -= sum_{k<j0} L(i,k) L(J,k) for the thread's rows
+                for (int i = j0 + tid; i < n; i += CT) {
+                    double acc[PNL];
+#pragma unroll
+                    for (int q = 0; q < PNL; ++q) acc[q] = (q < pw && j0 + q <= i) ? Lat(i, j0 + q) : 0.0;
+                    for (int k = 0; k < j0; ++k) {
+                        const double* col = Lp + OFF[k] - (k & ~1);
+                        const double lik = col[i];
+                        const double2* lj = reinterpret_cast<const double2*>(col + j0);
+#pragma unroll
+                        for (int q = 0; q < PNL; q += 2) {
+                            const double2 v = lj[q >> 1];
+                            acc[q] = fma(-lik, v.x, acc[q]);
+                            acc[q + 1] = fma(-lik, v.y, acc[q + 1]);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < PNL; ++q)
+                        if (q < pw && j0 + q <= i) Lat(i, j0 + q) = acc[q];
+                }
+                __syncthreads();
+                // phase 2: factor the diagonal block redundantly, then the thread's rows
+                double d[PNL][PNL];
+#pragma unroll
+                for (int a = 0; a < PNL; ++a)
+#pragma unroll
+                    for (int b = 0; b < PNL; ++b)
+                        d[a][b] = (a < pw && b <= a) ? Lat(j0 + a, j0 + b) : 0.0;
+                double inv[PNL];
+#pragma unroll
+                for (int c = 0; c < PNL; ++c) {
+                    if (c < pw && ok) {
+                        double sdiag = d[c][c];
+#pragma unroll
+                        for (int k = 0; k < c; ++k) sdiag = fma(-d[c][k], d[c][k], sdiag);
+                        if (!(sdiag > 0.0)) {
+                            ok = false;
+                        } else {
+                            const double lcc = sqrt(sdiag);
+                            inv[c] = 1.0 / lcc;
+                            d[c][c] = lcc;
+#pragma unroll
+                            for (int r = c + 1; r < PNL; ++r) {
+                                double v = d[r][c];
+#pragma unroll
+                                for (int k = 0; k < c; ++k) v = fma(-d[r][k], d[c][k], v);
+                                d[r][c] = v * inv[c];
+                            }
+                        }
+                    }
+                }
+                if (!ok) break;                          // uniform: same values in every thread
+                // rows below the block: L(i, J) = A(i, J) L_JJ^-T
+                for (int i = j0 + pw + tid; i < n; i += CT) {
+                    double v[PNL];
+#pragma unroll
+                    for (int c = 0; c < PNL; ++c) {
+                        if (c < pw) {
+                            double t = Lat(i, j0 + c);
+#pragma unroll
+                            for (int k = 0; k < c; ++k) t = fma(-v[k], d[c][k], t);
+                            v[c] = t * inv[c];
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < PNL; ++c)
+                        if (c < pw) Lat(i, j0 + c) = v[c];
+                }
+#pragma unroll
+                for (int a = 0; a < PNL; ++a) {          // static indices keep d[][] in registers
+                    if (a == tid && a < pw) {
+#pragma unroll
+                        for (int b = 0; b <= a; ++b) Lat(j0 + a, j0 + b) = d[a][b];
+                        INV[j0 + a] = inv[a];
+                    }
+                }
+                __syncthreads();
+            }
+            __syncthreads();
+        }
+        if (!ok) {
+            if (tid == 0) {
+                if constexpr (VOXEL) {
+                    va.cand_status[s] = VX_ST_CHOL_FAIL;
+                    const uint8_t st = va.state[vid];
+                    va.cand_before[s] = st;
+                    va.cand_after[s] = st;
+                } else {
+                    pa.status[s] = VX_ST_CHOL_FAIL;
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+
+        // ---- forward substitution in row chunks, one column per thread
+        const int ncols = m + 1;
+        const int wld = lay.wld;
+        const double* EA = base + lay.EA;
+        const double* EB = base + lay.EB;
+        for (int c0 = 0; c0 < ncols; c0 += wld) {
+            const int c = c0 + tid;
+            const bool active = tid < wld && c < ncols;
+            const int q = c - 1;
+            double g0 = 0, g1 = 0;
+            int ri = 0, si = 0;
+            if (active && c > 0) {
+                if constexpr (VOXEL) {
+                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+                    const int sr = q / (ns * nr2);
+                    const int rem = q - sr * ns * nr2;
+                    const int sc = rem / nr2;
+                    const int rem2 = rem - sc * nr2;
+                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                    ri = sr * nr + fr;
+                    si = sc * nr + fc;
+                    g0 = xadd(lo0, xdiv(xmul(double(ri) + 0.5, sp0), double(mm)));
+                    g1 = xadd(lo1, xdiv(xmul(double(si) + 0.5, sp1), double(mm)));
+                } else {
+                    g0 = pa.xs[(qo + q) * 2];
+                    g1 = pa.xs[(qo + q) * 2 + 1];
+                }
+            }
+            double ss = 0.0;
+            if (active) {
+                for (int k0 = 0; k0 < n; k0 += CH) {
+                    double acc[CH];
+#pragma unroll
+                    for (int r = 0; r < CH; ++r) {
+                        const int i = k0 + r;
+                        double v = 0.0;
+                        if (i < n) {
+                            if (c == 0) v = F[i];
+                            else if (VOXEL && kind == VX_KERNEL_SE) v = EA[i * mm + ri] * EB[i * mm + si];
+                            else v = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], g0, g1));
+                        }
+                        acc[r] = v;
+                    }
+                    for (int j = 0; j < k0; ++j) {
+                        const double wj = W[int64_t(j) * wld + tid];
+                        const double2* lc =
+                            reinterpret_cast<const double2*>(Lp + OFF[j] - (j & ~1) + k0);
+#pragma unroll
+                        for (int r = 0; r < CH; r += 2) {
+                            const double2 l2 = lc[r >> 1];
+                            acc[r] = fma(-l2.x, wj, acc[r]);
+                            acc[r + 1] = fma(-l2.y, wj, acc[r + 1]);
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < CH; ++r) {
+                        const int i = k0 + r;
+                        if (i < n) {
+                            const double w = acc[r] * INV[i];
+                            const double* lc = Lp + OFF[i] - (i & ~1) + k0;   // column i, rows k0..
+#pragma unroll
+                            for (int r2 = (r + 1) & ~1; r2 < CH; r2 += 2) {
+                                const double2 l2 = *reinterpret_cast<const double2*>(lc + r2);
+                                acc[r2] = fma(-l2.x, w, acc[r2]);
+                                acc[r2 + 1] = fma(-l2.y, w, acc[r2 + 1]);
+                            }
+                            acc[r] = w;
+                            ss = fma(w, w, ss);
+                            W[int64_t(i) * wld + tid] = w;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            if (c0 == 0 && tid == 0) {
+                for (int i = 0; i < n; ++i) NZ[i] = W[int64_t(i) * wld];   // z = L^-1 f
+            }
+            __syncthreads();
+            if (active && c > 0) {
+                double mu0 = 0.0, mu1 = 0.0;
+                int i = 0;
+                for (; i + 1 < n; i += 2) {
+                    mu0 = fma(W[int64_t(i) * wld + tid], NZ[i], mu0);
+                    mu1 = fma(W[int64_t(i + 1) * wld + tid], NZ[i + 1], mu1);
+                }
+                if (i < n) mu0 = fma(W[int64_t(i) * wld + tid], NZ[i], mu0);
+                const double mu = mu0 + mu1;
+                const double var = 1.0 - ss;
+                if constexpr (VOXEL) {
+                    base[lay.MU + q] = xadd(mu, mean_f);
+                    base[lay.VAR + q] = var < 0.0 ? 0.0 : var;
+                    double best = INFINITY;
+                    int bi = 0;
+                    for (int t = 0; t < n; ++t) {
+                        const double d2 = dist2_exact(g0, g1, X[2 * t], X[2 * t + 1]);
+                        if (d2 < best) { best = d2; bi = t; }
+                    }
+                    reinterpret_cast<int*>(base + lay.BI)[q] = bi;
+                } else {
+                    pa.mu[qo + q] = mu;
+                    pa.var[qo + q] = var;
+                }
+            }
+            __syncthreads();
+        }
+        if constexpr (VOXEL) {
+            double* COL = base + lay.COL;
+            const int* BI = reinterpret_cast<const int*>(base + lay.BI);
+            for (int q = tid; q < m; q += CT) {
+                const int bi = BI[q];
+                const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
+                                            : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
+                COL[q * 3] = cs[0];
+                COL[q * 3 + 1] = cs[1];
+                COL[q * 3 + 2] = cs[2];
+            }
+            __syncthreads();
+            const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
+            double* oxyz = va.pred_xyz + int64_t(slot) * m * 3;
+            double* orgb = va.pred_rgb + int64_t(slot) * m * 3;
+            double* ovar = va.pred_var + int64_t(slot) * m;
+            const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+            for (int q = tid; q < m; q += CT) {
+                const int sr = q / (ns * nr2);
+                const int rem = q - sr * ns * nr2;
+                const int sc = rem / nr2;
+                const int rem2 = rem - sc * nr2;
+                const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                double pos[3];
+                pos[axis] = base[lay.MU + q];
+                pos[pa_] = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
+                pos[pb_] = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
+                oxyz[q * 3] = pos[0];
+                oxyz[q * 3 + 1] = pos[1];
+                oxyz[q * 3 + 2] = pos[2];
+                orgb[q * 3] = COL[q * 3];
+                orgb[q * 3 + 1] = COL[q * 3 + 1];
+                orgb[q * 3 + 2] = COL[q * 3 + 2];
+                ovar[q] = base[lay.VAR + q];
+            }
+            if (tid == 0) {
+                const double* V = base + lay.VAR;
+                const double mv = xdiv(np_pairwise_sum([V](int i) { return V[i]; }, m), double(m));
+                const uint8_t before = va.state[vid];
+                const uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
+                va.state[vid] = after;
+                va.value_axis[vid] = int8_t(axis);
+                va.has_pred[vid] = 1;
+                va.cand_status[s] = VX_ST_OK;
+                va.cand_before[s] = before;
+                va.cand_after[s] = after;
+            }
+        } else {
+            if (tid == 0) pa.status[s] = VX_ST_OK;
+        }
+        __syncthreads();
+    }
+}
+
+template <bool VOXEL>
+static int launch_cta(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int n_max,
+                      int m_max, int mm, DevBuf& work, cudaStream_t s) {
+    if (num_items <= 0) return VX_OK;
+    const CtaLayout lay(n_max, mm, m_max, VOXEL);
+    const size_t bytes = size_t(lay.total) * sizeof(double);
+    auto kfn = gpr_cta_kernel<VOXEL>;
+    int blocks = num_items;
+    double* gw = nullptr;
+    size_t smem = 0;
+    if (bytes <= size_t(220) * 1024) {
+        smem = bytes;
+        VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int per_sm = int((size_t(227) * 1024) / (smem + 1024));
+        if (per_sm < 1) per_sm = 1;
+        if (per_sm > 8) per_sm = 8;
+        const int cap = sm_count() * per_sm;
+        if (blocks > cap) blocks = cap;
+    } else {
+        int cap = sm_count() * 2;
+        const int64_t max_blocks = (int64_t(4) << 30) / int64_t(bytes);
+        if (cap > max_blocks) cap = int(max_blocks > 0 ? max_blocks : 1);
+        if (blocks > cap) blocks = cap;
+        VX_TRY(work.reserve(bytes * blocks, s));
+        gw = work.as<double>();
+    }
+    kfn<<<blocks, CT, smem, s>>>(va, pa, n_max, m_max, mm, gw, int64_t(lay.total));
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 template <int NMAX, bool VOXEL>
@@ -860,7 +1309,9 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 0: return launch_warp<16, true>(a, none, a.num_items, a.M, mm, s);
         case 1: return launch_warp<32, true>(a, none, a.num_items, a.M, mm, s);
         case 2: return launch_warp<64, true>(a, none, a.num_items, a.M, mm, s);
-        default: return launch_generic<true>(a, none, a.num_items, max_n, a.M, work, s);
+        case 3: return launch_cta<true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm,
+                                        work, s);
+        default: return launch_cta<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
     }
 }
 
@@ -875,6 +1326,9 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
         if (bucket == 0) return launch_warp<16, false>(none, pa, count, max_m, 1, s);
         if (bucket == 1) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
         if (bucket == 2) return launch_warp<64, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 3) return launch_cta<false>(none, pa, count, max_n < 128 ? max_n : 128, max_m, 1,
+                                                  work, s);
+        return launch_cta<false>(none, pa, count, max_n, max_m, 1, work, s);
     }
     return launch_generic<false>(none, pa, count, max_n, max_m, work, s);
 }

@@ -77,9 +77,9 @@ enum {
     C_S,              // densify candidates
     C_MAXN,
     C_NEWSLOTS,
-    C_B0, C_B1, C_B2, C_B3,   // bucket counts
-    C_F0, C_F1, C_F2, C_F3,   // bucket fill cursors
-    C_O0, C_O1, C_O2, C_O3,   // bucket bases
+    C_B0, C_B1, C_B2, C_B3, C_B4,   // bucket counts
+    C_F0, C_F1, C_F2, C_F3, C_F4,   // bucket fill cursors
+    C_O0, C_O1, C_O2, C_O3, C_O4,   // bucket bases
     C_OK, C_DEGEN, C_CHOL, C_FIRST, C_CONV,
     C_COUNT
 };
