@@ -1203,6 +1203,483 @@ __global__ void __launch_bounds__(CT) gpr_cta_kernel(VoxelSolveArgs va, ProblemA
     }
 }
 
+// ---------------------------------------------------------------------------
+// DMMA tile kernel (33 <= n <= 128): FP64 tensor cores (mma.m8n8k4.f64)
+// ---------------------------------------------------------------------------
+// One voxel per CTA of NW warps.  The training set is padded to n8 = 8*ceil(n/8)
+// rows with an identity block (padding rows have zero right-hand sides, so they
+// do not change any result).  A lives column-major in shared memory (LD = n8+4
+// keeps DMMA fragment loads at two wavefronts).
+//  Cholesky: left-looking by 8-column panels.  The panel update
+//    A(i >= j0, J) -= L(i, <j0) L(J, <j0)^T is a GEMM done with DMMA 8x8x4
+//    (row tiles spread over the warps); warp 0 factors the 8x8 diagonal block
+//    with shuffles (dpotrf failure rule); the rows below are solved against it.
+//  Forward substitution: right-looking with the whole right-hand-side block
+//    resident in registers as DMMA accumulators: warp w owns CTW column tiles
+//    (8 columns each) of [f | K*]; for each row block k it solves the 8x8
+//    diagonal system with shuffles, converts W_k to B fragments and updates all
+//    later row blocks with DMMA.  No shared-memory W, no CTA barrier inside.
+__device__ __forceinline__ void dmma_acc(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+struct TileLayout {
+    int L, X, F, NZ, INV, Z, EA, EB, MU, VAR, BI, COL, FLAG, total, ld;
+    __host__ __device__ TileLayout(int N8, int mm, int mcols, int mmax, bool voxel) {
+        ld = N8 + 4;
+        int o = 0;
+        L = o; o += N8 * ld;
+        X = o; o += 2 * N8;
+        F = o; o += N8;
+        NZ = o; o += N8;
+        INV = o; o += N8;
+        Z = o; o += N8;
+        EA = EB = MU = VAR = BI = COL = o;
+        if (voxel) {
+            EA = o; o += N8 * mm;
+            EB = o; o += N8 * mm;
+            COL = o; o += 3 * mmax + 1;
+        }
+        MU = o; o += mcols;
+        VAR = o; o += mcols;
+        BI = o; o += mcols;
+        FLAG = o; o += 2;
+        total = (o + 1) & ~1;
+    }
+};
+
+template <int NRB, int CTW, int NW, bool VOXEL>
+__global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
+                                                           int mmax, int mm) {
+    extern __shared__ __align__(16) double smem[];
+    constexpr int N8 = NRB * 8;
+    constexpr int NT = NW * 32;
+    constexpr int PCOLS = NW * CTW * 8;             // right-hand sides per pass
+    const TileLayout lay(N8, mm, PCOLS, mmax, VOXEL);
+    const int LDL = lay.ld;
+    double* L = smem + lay.L;
+    double* X = smem + lay.X;
+    double* F = smem + lay.F;
+    double* NZ = smem + lay.NZ;
+    double* INV = smem + lay.INV;
+    double* Z = smem + lay.Z;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, tig = lane & 3;
+    const int num_items = VOXEL ? va.num_items : pa.num_items;
+
+    for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
+        int n, m, s, vid = 0, cnt = 0, slot = 0, axis = 2;
+        int64_t off = 0, xo = 0, qo = 0;
+        double lam, jitter, mean_f = 0.0;
+        int kind;
+        double lo0 = 0, lo1 = 0, sp0 = 0, sp1 = 0;
+        if constexpr (VOXEL) {
+            s = va.items[it];
+            vid = va.cand_voxel[s];
+            n = va.cand_n[s];
+            cnt = va.raw_count[vid];
+            off = va.raw_offset[vid];
+            slot = va.pred_slot[vid];
+            m = va.M;
+            lam = va.lam;
+            jitter = va.jitter;
+            kind = va.kernel;
+            axis = va.cand_axis[s];
+            mean_f = va.cand_meanf[s];
+            const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
+            for (int r = tid; r < N8; r += NT) {
+                if (r < n) {
+                    const double* p = train_point(va, r, cnt, off, slot);
+                    X[2 * r] = p[pa_];
+                    X[2 * r + 1] = p[pb_];
+                    F[r] = xsub(p[axis], mean_f);
+                    NZ[r] = r < cnt ? va.sensor_var : va.pred_var[int64_t(slot) * m + (r - cnt)];
+                } else {
+                    X[2 * r] = X[2 * r + 1] = F[r] = NZ[r] = 0.0;
+                }
+            }
+            lo0 = xmul(double(va.keys[int64_t(vid) * 3 + pa_]), va.voxel_size);
+            lo1 = xmul(double(va.keys[int64_t(vid) * 3 + pb_]), va.voxel_size);
+            sp0 = xsub(xadd(lo0, va.voxel_size), lo0);
+            sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
+            __syncthreads();
+            if (kind == VX_KERNEL_SE) {
+                double* EA = smem + lay.EA;
+                double* EB = smem + lay.EB;
+                for (int e = tid; e < 2 * N8 * mm; e += NT) {
+                    const int which = e >= N8 * mm;
+                    const int rem = e - which * N8 * mm;
+                    const int i = rem / mm, r = rem - i * mm;
+                    double v = 0.0;
+                    if (i < n) {
+                        const double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
+                        const double gg = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
+                        const double d = xsub(X[2 * i + which], gg);
+                        v = exp(xmul(-lam, xmul(d, d)));
+                    }
+                    (which ? EB : EA)[i * mm + r] = v;
+                }
+            }
+        } else {
+            s = pa.items[it];
+            xo = pa.x_off[s];
+            qo = pa.q_off[s];
+            n = int(pa.x_off[s + 1] - xo);
+            m = int(pa.q_off[s + 1] - qo);
+            lam = pa.lam[s];
+            jitter = pa.jitter;
+            kind = pa.kernel;
+            for (int r = tid; r < N8; r += NT) {
+                if (r < n) {
+                    X[2 * r] = pa.x[(xo + r) * 2];
+                    X[2 * r + 1] = pa.x[(xo + r) * 2 + 1];
+                    F[r] = pa.f[xo + r];
+                    NZ[r] = pa.noise[xo + r];
+                } else {
+                    X[2 * r] = X[2 * r + 1] = F[r] = NZ[r] = 0.0;
+                }
+            }
+        }
+        const int nrb = (n + 7) >> 3;
+        const int n8 = nrb * 8;
+        __syncthreads();
+
+        // ---- A (identity-padded), panel Cholesky with DMMA updates, one retry
+        bool ok = false;
+        for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+            const double jit = attempt ? jitter : 0.0;
+            const int tot = n8 * (n8 + 1) / 2;
+            for (int e = tid; e < tot; e += NT) {
+                int i, j;
+                tri_decode(e, &i, &j);
+                double v;
+                if (i >= n) {
+                    v = (i == j) ? 1.0 : 0.0;
+                } else if (i == j) {
+                    v = xadd(1.0, NZ[i]);
+                    if (jit != 0.0) v = xadd(v, jit);
+                } else {
+                    v = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
+                }
+                L[j * LDL + i] = v;
+            }
+            __syncthreads();
+            ok = true;
+            for (int kb = 0; kb < nrb; ++kb) {
+                const int j0 = kb * 8;
+                // (a) panel update A(i, J) -= L(i, <j0) L(J, <j0)^T, row tiles over warps
+                if (j0 > 0) {
+                    for (int t = kb + warp; t < nrb; t += NW) {
+                        const int rb = t * 8;
+                        double c0 = L[(j0 + 2 * tig) * LDL + rb + g];
+                        double c1 = L[(j0 + 2 * tig + 1) * LDL + rb + g];
+                        for (int k4 = 0; k4 < j0; k4 += 4) {
+                            const double a = -L[(k4 + tig) * LDL + rb + g];
+                            const double b = L[(k4 + tig) * LDL + j0 + g];
+                            dmma_acc(c0, c1, a, b);
+                        }
+                        L[(j0 + 2 * tig) * LDL + rb + g] = c0;
+                        L[(j0 + 2 * tig + 1) * LDL + rb + g] = c1;
+                    }
+                    __syncthreads();
+                }
+                // (b) warp 0 factors the 8x8 diagonal block (lane r < 8 holds row r)
+                if (warp == 0) {
+                    double d[8];
+                    const int r = lane & 7;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) d[k] = (k <= r) ? L[(j0 + k) * LDL + j0 + r] : 0.0;
+                    bool okw = true;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const double piv = __shfl_sync(FULL, d[c], c);
+                        if (!(piv > 0.0)) okw = false;
+                        const double lcc = sqrt(piv);
+                        const double inv = 1.0 / lcc;
+                        if (r == c) d[c] = lcc;
+                        else if (r > c) d[c] = d[c] * inv;
+#pragma unroll
+                        for (int k = c + 1; k < 8; ++k) {
+                            const double lkc = __shfl_sync(FULL, d[c], k);
+                            if (r >= k) d[k] = fma(-d[c], lkc, d[k]);
+                        }
+                        if (lane == c) INV[j0 + c] = inv;
+                    }
+                    if (lane < 8) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            if (k <= r) L[(j0 + k) * LDL + j0 + r] = d[k];
+                    }
+                    if (lane == 0) smem[lay.FLAG] = okw ? 1.0 : 0.0;
+                }
+                __syncthreads();
+                if (smem[lay.FLAG] == 0.0) {
+                    ok = false;
+                    break;
+                }
+                // (c) rows below the block: L(i, J) = A(i, J) L_JJ^-T
+                for (int i = j0 + 8 + tid; i < n8; i += NT) {
+                    double v[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        double t = L[(j0 + c) * LDL + i];
+#pragma unroll
+                        for (int k = 0; k < c; ++k) t = fma(-v[k], L[(j0 + k) * LDL + j0 + c], t);
+                        v[c] = t * INV[j0 + c];
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) L[(j0 + c) * LDL + i] = v[c];
+                }
+                __syncthreads();
+            }
+            __syncthreads();
+        }
+        if (!ok) {
+            if (tid == 0) {
+                if constexpr (VOXEL) {
+                    va.cand_status[s] = VX_ST_CHOL_FAIL;
+                    const uint8_t st = va.state[vid];
+                    va.cand_before[s] = st;
+                    va.cand_after[s] = st;
+                } else {
+                    pa.status[s] = VX_ST_CHOL_FAIL;
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+
+        // ---- forward substitution: right-hand sides resident as DMMA accumulators
+        const int ncols = m + 1;
+        const double* EA = smem + lay.EA;
+        const double* EB = smem + lay.EB;
+        for (int c0 = 0; c0 < ncols; c0 += PCOLS) {
+            double C[NRB][CTW][2];
+            // right-hand side values: rows 8 rb + g, columns c0 + 8 (warp*CTW + ct) + 2 tig + e
+#pragma unroll
+            for (int ct = 0; ct < CTW; ++ct) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = c0 + (warp * CTW + ct) * 8 + 2 * tig + e;
+                    const int q = c - 1;
+                    int ri = 0, si = 0;
+                    double g0 = 0, g1 = 0;
+                    if (c > 0 && c < ncols) {
+                        if constexpr (VOXEL) {
+                            const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+                            const int sr = q / (ns * nr2);
+                            const int rem = q - sr * ns * nr2;
+                            const int sc = rem / nr2;
+                            const int rem2 = rem - sc * nr2;
+                            const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                            ri = sr * nr + fr;
+                            si = sc * nr + fc;
+                            g0 = xadd(lo0, xdiv(xmul(double(ri) + 0.5, sp0), double(mm)));
+                            g1 = xadd(lo1, xdiv(xmul(double(si) + 0.5, sp1), double(mm)));
+                        } else {
+                            g0 = pa.xs[(qo + q) * 2];
+                            g1 = pa.xs[(qo + q) * 2 + 1];
+                        }
+                    }
+#pragma unroll
+                    for (int rb = 0; rb < NRB; ++rb) {
+                        const int i = rb * 8 + g;
+                        double v = 0.0;
+                        if (rb < nrb && i < n && c < ncols) {
+                            if (c == 0) v = F[i];
+                            else if (VOXEL && kind == VX_KERNEL_SE) v = EA[i * mm + ri] * EB[i * mm + si];
+                            else v = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], g0, g1));
+                        }
+                        C[rb][ct][e] = v;
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NRB; ++k) {
+                if (k < nrb) {
+                    // diagonal 8x8 solve on row block k (row g of the block lives in lane group g)
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const double inv = INV[k * 8 + r];
+                        const double lgr = (g > r) ? L[(k * 8 + r) * LDL + k * 8 + g] : 0.0;
+#pragma unroll
+                        for (int ct = 0; ct < CTW; ++ct) {
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                if (g == r) C[k][ct][e] *= inv;
+                                const double wr = __shfl_sync(FULL, C[k][ct][e], r * 4 + tig);
+                                if (g > r) C[k][ct][e] = fma(-lgr, wr, C[k][ct][e]);
+                            }
+                        }
+                    }
+                    if (k + 1 < nrb) {
+                        // W_k as B fragments: B_s[tig][g] = W(8k + 4s + tig, col 8ct + g)
+                        double bf[CTW][2];
+#pragma unroll
+                        for (int ct = 0; ct < CTW; ++ct) {
+#pragma unroll
+                            for (int sl = 0; sl < 2; ++sl) {
+                                const int src = (4 * sl + tig) * 4 + (g >> 1);
+                                const double v0 = __shfl_sync(FULL, C[k][ct][0], src);
+                                const double v1 = __shfl_sync(FULL, C[k][ct][1], src);
+                                bf[ct][sl] = (g & 1) ? v1 : v0;
+                            }
+                        }
+#pragma unroll
+                        for (int k2 = k + 1; k2 < NRB; ++k2) {
+                            if (k2 < nrb) {
+#pragma unroll
+                                for (int sl = 0; sl < 2; ++sl) {
+                                    const double a = -L[(k * 8 + 4 * sl + tig) * LDL + k2 * 8 + g];
+#pragma unroll
+                                    for (int ct = 0; ct < CTW; ++ct)
+                                        dmma_acc(C[k2][ct][0], C[k2][ct][1], a, bf[ct][sl]);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            // z = L^-1 f (global column 0) to shared memory
+            if (c0 == 0 && warp == 0 && tig == 0) {
+#pragma unroll
+                for (int rb = 0; rb < NRB; ++rb)
+                    if (rb < nrb) Z[rb * 8 + g] = C[rb][0][0];
+            }
+            __syncthreads();
+            // per-column sum of squares and mu = w . z, reduced over the row groups g
+#pragma unroll
+            for (int ct = 0; ct < CTW; ++ct) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    double ss = 0.0, mu = 0.0;
+#pragma unroll
+                    for (int rb = 0; rb < NRB; ++rb) {
+                        if (rb < nrb) {
+                            const double w = C[rb][ct][e];
+                            ss = fma(w, w, ss);
+                            mu = fma(w, Z[rb * 8 + g], mu);
+                        }
+                    }
+#pragma unroll
+                    for (int o = 4; o < 32; o <<= 1) {
+                        ss += __shfl_xor_sync(FULL, ss, o);
+                        mu += __shfl_xor_sync(FULL, mu, o);
+                    }
+                    const int lc = (warp * CTW + ct) * 8 + 2 * tig + e;   // column within the pass
+                    const int c = c0 + lc;
+                    if (g == 0 && c > 0 && c < ncols) {
+                        const double var = 1.0 - ss;
+                        if constexpr (VOXEL) {
+                            smem[lay.MU + lc] = xadd(mu, mean_f);
+                            smem[lay.VAR + lc] = var < 0.0 ? 0.0 : var;
+                        } else {
+                            pa.mu[qo + c - 1] = mu;
+                            pa.var[qo + c - 1] = var;
+                        }
+                    }
+                }
+            }
+            if constexpr (VOXEL) {
+                // voxel mode: m + 1 <= PCOLS (asserted by the launcher), one pass
+                __syncthreads();
+                double* COL = smem + lay.COL;
+                int* BI = reinterpret_cast<int*>(smem + lay.BI);
+                for (int q = tid; q < m; q += NT) {
+                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+                    const int sr = q / (ns * nr2);
+                    const int rem = q - sr * ns * nr2;
+                    const int sc = rem / nr2;
+                    const int rem2 = rem - sc * nr2;
+                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                    const double g0 = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
+                    const double g1 = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
+                    double best = INFINITY;
+                    int bi = 0;
+                    for (int t = 0; t < n; ++t) {
+                        const double d2 = dist2_exact(g0, g1, X[2 * t], X[2 * t + 1]);
+                        if (d2 < best) { best = d2; bi = t; }
+                    }
+                    BI[q] = bi;
+                    const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
+                                                : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
+                    COL[q * 3] = cs[0];
+                    COL[q * 3 + 1] = cs[1];
+                    COL[q * 3 + 2] = cs[2];
+                }
+                __syncthreads();
+                const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
+                double* oxyz = va.pred_xyz + int64_t(slot) * m * 3;
+                double* orgb = va.pred_rgb + int64_t(slot) * m * 3;
+                double* ovar = va.pred_var + int64_t(slot) * m;
+                for (int q = tid; q < m; q += NT) {
+                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+                    const int sr = q / (ns * nr2);
+                    const int rem = q - sr * ns * nr2;
+                    const int sc = rem / nr2;
+                    const int rem2 = rem - sc * nr2;
+                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                    double pos[3];
+                    pos[axis] = smem[lay.MU + q + 1];
+                    pos[pa_] = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
+                    pos[pb_] = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
+                    oxyz[q * 3] = pos[0];
+                    oxyz[q * 3 + 1] = pos[1];
+                    oxyz[q * 3 + 2] = pos[2];
+                    orgb[q * 3] = COL[q * 3];
+                    orgb[q * 3 + 1] = COL[q * 3 + 1];
+                    orgb[q * 3 + 2] = COL[q * 3 + 2];
+                    ovar[q] = smem[lay.VAR + q + 1];
+                }
+                if (tid == 0) {
+                    const double* V = smem + lay.VAR + 1;
+                    const double mv = xdiv(np_pairwise_sum([V](int i) { return V[i]; }, m), double(m));
+                    const uint8_t before = va.state[vid];
+                    const uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
+                    va.state[vid] = after;
+                    va.value_axis[vid] = int8_t(axis);
+                    va.has_pred[vid] = 1;
+                    va.cand_status[s] = VX_ST_OK;
+                    va.cand_before[s] = before;
+                    va.cand_after[s] = after;
+                }
+            }
+            __syncthreads();
+        }
+        if constexpr (!VOXEL) {
+            if (tid == 0) pa.status[s] = VX_ST_OK;
+        }
+        __syncthreads();
+    }
+}
+
+template <int NRB, int CTW, int NW, bool VOXEL>
+static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int m_max,
+                       int mm, cudaStream_t s) {
+    if (num_items <= 0) return VX_OK;
+    constexpr int PCOLS = NW * CTW * 8;
+    if (VOXEL && m_max + 1 > PCOLS) {
+        set_error("tile kernel: %d right-hand sides exceed %d", m_max + 1, PCOLS);
+        return VX_E_INPUT;
+    }
+    const TileLayout lay(NRB * 8, mm, PCOLS, m_max, VOXEL);
+    const size_t smem = size_t(lay.total) * sizeof(double);
+    auto kfn = gpr_tile_kernel<NRB, CTW, NW, VOXEL>;
+    VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = int((size_t(227) * 1024) / (smem + 1024));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 8) per_sm = 8;
+    int blocks = num_items;
+    const int cap = sm_count() * per_sm;
+    if (blocks > cap) blocks = cap;
+    kfn<<<blocks, NW * 32, smem, s>>>(va, pa, m_max, mm);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
 template <bool VOXEL>
 static int launch_cta(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int n_max,
                       int m_max, int mm, DevBuf& work, cudaStream_t s) {
@@ -1308,9 +1785,12 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
     switch (bucket) {
         case 0: return launch_warp<16, true>(a, none, a.num_items, a.M, mm, s);
         case 1: return launch_warp<32, true>(a, none, a.num_items, a.M, mm, s);
-        case 2: return launch_warp<64, true>(a, none, a.num_items, a.M, mm, s);
-        case 3: return launch_cta<true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm,
-                                        work, s);
+        case 2:
+            if (a.M + 1 <= 96) return launch_tile<8, 3, 4, true>(a, none, a.num_items, a.M, mm, s);
+            return launch_warp<64, true>(a, none, a.num_items, a.M, mm, s);
+        case 3:
+            if (a.M + 1 <= 96) return launch_tile<16, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
+            return launch_cta<true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
         default: return launch_cta<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
     }
 }
@@ -1325,9 +1805,8 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
     if (b.d_full == nullptr) {
         if (bucket == 0) return launch_warp<16, false>(none, pa, count, max_m, 1, s);
         if (bucket == 1) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 2) return launch_warp<64, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 3) return launch_cta<false>(none, pa, count, max_n < 128 ? max_n : 128, max_m, 1,
-                                                  work, s);
+        if (bucket == 2) return launch_tile<8, 3, 4, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 3) return launch_tile<16, 2, 6, false>(none, pa, count, max_m, 1, s);
         return launch_cta<false>(none, pa, count, max_n, max_m, 1, work, s);
     }
     return launch_generic<false>(none, pa, count, max_n, max_m, work, s);
