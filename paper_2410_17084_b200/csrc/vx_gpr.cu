@@ -1226,11 +1226,13 @@ __device__ __forceinline__ void dmma_acc(double& c0, double& c1, double a, doubl
 }
 
 struct TileLayout {
-    int L, X, F, NZ, INV, Z, EA, EB, MU, VAR, BI, COL, FLAG, total, ld;
+    int L, LINV, LDG, X, F, NZ, INV, Z, EA, EB, MU, VAR, BI, COL, FLAG, total, ld;
     __host__ __device__ TileLayout(int N8, int mm, int mcols, int mmax, bool voxel) {
         ld = N8 + 4;
         int o = 0;
         L = o; o += N8 * ld;
+        LINV = o; o += N8 * 8;          // inverses of the 8x8 diagonal blocks, row-major
+        LDG = o; o += N8 * 8;           // factored 8x8 diagonal blocks, row-major
         X = o; o += 2 * N8;
         F = o; o += N8;
         NZ = o; o += N8;
@@ -1265,6 +1267,7 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
     double* NZ = smem + lay.NZ;
     double* INV = smem + lay.INV;
     double* Z = smem + lay.Z;
+    double* LDG = smem + lay.LDG;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, tig = lane & 3;
     const int num_items = VOXEL ? va.num_items : pa.num_items;
@@ -1350,10 +1353,9 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
         bool ok = false;
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? jitter : 0.0;
-            const int tot = n8 * (n8 + 1) / 2;
-            for (int e = tid; e < tot; e += NT) {
-                int i, j;
-                tri_decode(e, &i, &j);
+            for (int e = tid; e < n8 * n8; e += NT) {
+                const int j = e / n8, i = e - j * n8;      // column-major: coalesced rows
+                if (i < j) continue;
                 double v;
                 if (i >= n) {
                     v = (i == j) ? 1.0 : 0.0;
@@ -1385,8 +1387,11 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                     }
                     __syncthreads();
                 }
-                // (b) warp 0 factors the 8x8 diagonal block (lane r < 8 holds row r)
-                if (warp == 0) {
+                // (b) every warp factors the 8x8 diagonal block redundantly (lane r
+                // holds row r); identical inputs give identical outputs, so the
+                // duplicate shared-memory stores are benign and no barrier separates
+                // the factorisation from the rows below
+                {
                     double d[8];
                     const int r = lane & 7;
 #pragma unroll
@@ -1407,17 +1412,15 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                         }
                         if (lane == c) INV[j0 + c] = inv;
                     }
-                    if (lane < 8) {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            if (k <= r) L[(j0 + k) * LDL + j0 + r] = d[k];
+                    if (lane < 8) {                   // separate buffer: other warps may
+#pragma unroll                                        // still be reading the block in L
+                        for (int k = 0; k < 8; ++k) LDG[(j0 + r) * 8 + k] = (k <= r) ? d[k] : 0.0;
                     }
-                    if (lane == 0) smem[lay.FLAG] = okw ? 1.0 : 0.0;
-                }
-                __syncthreads();
-                if (smem[lay.FLAG] == 0.0) {
-                    ok = false;
-                    break;
+                    __syncwarp();
+                    if (!okw) {                       // uniform across the CTA
+                        ok = false;
+                        break;
+                    }
                 }
                 // (c) rows below the block: L(i, J) = A(i, J) L_JJ^-T
                 for (int i = j0 + 8 + tid; i < n8; i += NT) {
@@ -1426,7 +1429,7 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                     for (int c = 0; c < 8; ++c) {
                         double t = L[(j0 + c) * LDL + i];
 #pragma unroll
-                        for (int k = 0; k < c; ++k) t = fma(-v[k], L[(j0 + k) * LDL + j0 + c], t);
+                        for (int k = 0; k < c; ++k) t = fma(-v[k], LDG[(j0 + c) * 8 + k], t);
                         v[c] = t * INV[j0 + c];
                     }
 #pragma unroll
@@ -1450,6 +1453,22 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
             __syncthreads();
             continue;
         }
+        // inverses of the diagonal blocks (thread = (block, column)): L_kk x = e_c
+        double* LINV = smem + lay.LINV;
+        for (int t = tid; t < nrb * 8; t += NT) {
+            const int kb = t >> 3, c = t & 7, b0 = kb * 8;
+            double x[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                double v = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+                for (int k = 0; k < r; ++k) v = fma(-LDG[(b0 + r) * 8 + k], x[k], v);
+                x[r] = (r < c) ? 0.0 : v * INV[b0 + r];
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) LINV[(b0 + r) * 8 + c] = x[r];
+        }
+        __syncthreads();
 
         // ---- forward substitution: right-hand sides resident as DMMA accumulators
         const int ncols = m + 1;
@@ -1499,19 +1518,28 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
 #pragma unroll
             for (int k = 0; k < NRB; ++k) {
                 if (k < nrb) {
-                    // diagonal 8x8 solve on row block k (row g of the block lives in lane group g)
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        const double inv = INV[k * 8 + r];
-                        const double lgr = (g > r) ? L[(k * 8 + r) * LDL + k * 8 + g] : 0.0;
+                    // diagonal block: W_k = L_kk^-1 C_k with DMMA (C_k -> B fragments by shuffles)
+                    {
+                        double bc[CTW][2];
 #pragma unroll
                         for (int ct = 0; ct < CTW; ++ct) {
 #pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                if (g == r) C[k][ct][e] *= inv;
-                                const double wr = __shfl_sync(FULL, C[k][ct][e], r * 4 + tig);
-                                if (g > r) C[k][ct][e] = fma(-lgr, wr, C[k][ct][e]);
+                            for (int sl = 0; sl < 2; ++sl) {
+                                const int src = (4 * sl + tig) * 4 + (g >> 1);
+                                const double v0 = __shfl_sync(FULL, C[k][ct][0], src);
+                                const double v1 = __shfl_sync(FULL, C[k][ct][1], src);
+                                bc[ct][sl] = (g & 1) ? v1 : v0;
                             }
+                        }
+                        const double a0 = LINV[(k * 8 + g) * 8 + tig];
+                        const double a1 = LINV[(k * 8 + g) * 8 + 4 + tig];
+#pragma unroll
+                        for (int ct = 0; ct < CTW; ++ct) {
+                            double d0 = 0.0, d1 = 0.0;
+                            dmma_acc(d0, d1, a0, bc[ct][0]);
+                            dmma_acc(d0, d1, a1, bc[ct][1]);
+                            C[k][ct][0] = d0;
+                            C[k][ct][1] = d1;
                         }
                     }
                     if (k + 1 < nrb) {
