@@ -22,11 +22,18 @@ oracle/voxsplat_oracle.py) on a bounded sample with all host cores.
 
 from __future__ import annotations
 
+import os
+
+# The CPU legs (cpu_baseline, --impl reference) run P single-threaded oracle
+# processes; a multi-threaded BLAS per process is ~8x slower on these small
+# solves.  Must be set before NumPy/SciPy load OpenBLAS.
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import argparse
 import json
 import math
 import multiprocessing as mp
-import os
 import subprocess
 import sys
 import time
@@ -126,8 +133,6 @@ class Clocks:
 
 def _oracle_worker(args):
     pos, col, cam, img, cfg = args
-    from threadpoolctl import threadpool_limits
-    threadpool_limits(1)          # one BLAS thread per process (no oversubscription)
     from oracle import voxsplat_oracle as O
     omap = O.OracleMap(0.5, 1e-4, TAU, 0.3)
     ocam = O.OracleCamera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], cam["width"],
@@ -342,7 +347,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--voxels", type=int, default=1_000_000)
-    ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--ref-sample", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -1353,9 +1353,13 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
         bool ok = false;
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? jitter : 0.0;
-            for (int e = tid; e < n8 * n8; e += NT) {
-                const int j = e / n8, i = e - j * n8;      // column-major: coalesced rows
-                if (i < j) continue;
+            const int tot = n8 * (n8 + 1) / 2;
+            for (int e = tid; e < tot; e += NT) {
+                // lower-triangle index -> (i, j): single-precision root + one fix-up
+                int i = int((sqrtf(8.0f * float(e) + 1.0f) - 1.0f) * 0.5f);
+                if ((i + 1) * (i + 2) / 2 <= e) ++i;
+                if (i * (i + 1) / 2 > e) --i;
+                const int j = e - i * (i + 1) / 2;
                 double v;
                 if (i >= n) {
                     v = (i == j) ? 1.0 : 0.0;
