@@ -286,9 +286,10 @@ def run_gpu(args, rank, world, local_rank):
     top = max(stages, key=lambda k: stages[k][0])
     top_ms, top_n = stages[top]
     sol = counts[counts >= TAU]
-    bucket = {"gpr_warp16": sol[sol <= 16], "gpr_warp32": sol[(sol > 16) & (sol <= 32)],
-              "gpr_warp64": sol[(sol > 32) & (sol <= 64)],
-              "gpr_cta128": sol[(sol > 64) & (sol <= 128)], "gpr_cta_large": sol[sol > 128]}
+    bucket = {"gpr_warp16": sol[sol <= 16], "gpr_warp24": sol[(sol > 16) & (sol <= 24)],
+              "gpr_warp32": sol[(sol > 24) & (sol <= 32)],
+              "gpr_tile64": sol[(sol > 32) & (sol <= 64)],
+              "gpr_tile128": sol[(sol > 64) & (sol <= 128)], "gpr_cta_large": sol[sol > 128]}
     if top in bucket:
         flops = float(gpr_flops(bucket[top]).sum()) * args.steps
         achieved = flops / (top_ms / 1e3) / 1e12

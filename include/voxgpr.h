@@ -215,6 +215,9 @@ typedef struct {
     const int64_t* raw_offset;     /* (V)   row of the voxel's first raw point */
     const int32_t* pred_slot;      /* (V)   -1 = no prediction yet */
     const uint8_t* has_pred;       /* (V)   */
+    const int32_t* last_first;     /* (V)   index of the voxel's first point in the
+                                              last frame that touched it (global order key
+                                              for gathering sharded outputs) */
     const double* raw_xyz;         /* arena (.,3) */
     const double* raw_rgb;         /* arena (.,3) */
     int64_t pred_points;           /* M = (n_s n_r)^2 */
@@ -304,9 +307,9 @@ int vx_init_color(const double* d_positions, const double* d_fallback, int64_t n
 int vx_fp64_peak(double* tflops, void* stream);
 
 /* CUDA-event timers around the library's stages, recorded on the launching
- * stream: 0 store_frame (hashing), 1-3 GPR warp kernels n<=16/32/64,
- * 4-5 GPR CTA kernels n<=128 / n>128, 6 Gaussian init, 7 whole densify,
- * 8 PCA prepass.  vx_profile(1) resets
+ * stream: 0 store_frame (hashing), 1-2 GPR warp kernels n<=16/24,
+ * 3-4 GPR DMMA tile kernels n<=64/128, 5 GPR CTA kernel n>128, 6 warp kernel
+ * n<=32, 7 Gaussian init, 8 whole densify, 9 PCA prepass.  vx_profile(1) resets
  * and enables; vx_profile_read fills total ms and launch counts per stage
  * and returns the number of stages. */
 int vx_profile(int enable);

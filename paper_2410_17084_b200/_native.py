@@ -81,6 +81,7 @@ class VxDensifyInfo(C.Structure):
 class VxMapView(C.Structure):
     _fields_ = [("num_voxels", C.c_int64), ("keys", vp), ("state", vp), ("value_axis", vp),
                 ("raw_count", vp), ("raw_offset", vp), ("pred_slot", vp), ("has_pred", vp),
+                ("last_first", vp),
                 ("raw_xyz", vp), ("raw_rgb", vp), ("pred_points", C.c_int64), ("pred_xyz", vp),
                 ("pred_rgb", vp), ("pred_var", vp), ("frame_touched", C.c_int64),
                 ("frame_voxels", vp), ("frame_state_before", vp), ("frame_state_after", vp),
@@ -258,8 +259,8 @@ def splat_struct(n_s, n_r, weight_floor, scale_floor, opacity, rotation="identit
     return s
 
 
-PROFILE_STAGES = ("hash", "gpr_warp16", "gpr_warp32", "gpr_warp64", "gpr_cta128", "gpr_cta_large",
-                  "splat", "densify", "pca")
+PROFILE_STAGES = ("hash", "gpr_warp16", "gpr_warp24", "gpr_tile64", "gpr_tile128", "gpr_cta_large",
+                  "gpr_warp32", "splat", "densify", "pca")
 
 
 def profile(enable: bool) -> None:

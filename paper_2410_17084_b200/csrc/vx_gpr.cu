@@ -227,14 +227,21 @@ __global__ void __launch_bounds__(128) gpr_warp_kernel(VoxelSolveArgs va, Proble
             if (kind == VX_KERNEL_SE) {
                 double* EA = base + lay.EA;
                 double* EB = base + lay.EB;
-                for (int e = lane; e < 2 * n * mm; e += 32) {
-                    const int which = e >= n * mm;
-                    const int rem = e - which * n * mm;
-                    const int i = rem / mm, r = rem - i * mm;
+                // lane = (table, training row); rows >= n get zeros (padding)
+                for (int e = lane; e < 2 * NMAX; e += 32) {
+                    const int which = e / NMAX, i = e - which * NMAX;
                     const double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
-                    const double g = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
-                    const double d = xsub(X[2 * i + which], g);
-                    (which ? EB : EA)[i * mm + r] = exp(xmul(-lam, xmul(d, d)));
+                    double* T = (which ? EB : EA) + i * mm;
+                    if (i < n) {
+                        const double xi = X[2 * i + which];
+                        for (int r = 0; r < mm; ++r) {
+                            const double g = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
+                            const double d = xsub(xi, g);
+                            T[r] = exp(xmul(-lam, xmul(d, d)));
+                        }
+                    } else {
+                        for (int r = 0; r < mm; ++r) T[r] = 0.0;
+                    }
                 }
             }
         } else {
@@ -259,20 +266,25 @@ __global__ void __launch_bounds__(128) gpr_warp_kernel(VoxelSolveArgs va, Proble
         bool ok = false;
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? jitter : 0.0;
-            const int tot = n * (n + 1) / 2;
-            for (int e = lane; e < tot; e += 32) {
-                int i, j;
-                tri_decode(e, &i, &j);
-                double v;
-                if (i == j) {
-                    v = xadd(1.0, NZ[i]);          // K_ii = exp(-lam*0) = 1, + noise
-                    if (jit != 0.0) v = xadd(v, jit);
-                } else {
-                    v = kernel_value(kind, lam,
-                                     dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
+            // whole NMAX x NMAX column-major square: the live lower triangle, zeros
+            // elsewhere, so the forward substitution can run unguarded on
+            // padding rows (their right-hand sides and 1/L_ii are zero)
+            for (int e = lane; e < NMAX * NMAX; e += 32) {
+                const int j = e / NMAX, i = e - j * NMAX;
+                double v = 0.0;
+                if (i < n && j <= i) {
+                    if (i == j) {
+                        v = xadd(1.0, NZ[i]);          // K_ii = exp(-lam*0) = 1, + noise
+                        if (jit != 0.0) v = xadd(v, jit);
+                    } else {
+                        v = kernel_value(kind, lam,
+                                         dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
+                    }
                 }
-                L[j * LD + i] = v;                 // column-major lower triangle
+                L[e] = v;
             }
+            if (lane < NMAX) INV[lane] = 0.0;
+            if (NMAX > 32 && lane + 32 < NMAX) INV[lane + 32] = 0.0;
             __syncwarp();
             ok = true;
             for (int j = 0; j < n; ++j) {
@@ -297,8 +309,8 @@ __global__ void __launch_bounds__(128) gpr_warp_kernel(VoxelSolveArgs va, Proble
                     ok = false;
                     break;
                 }
-                const double ljj = sqrt(d);
-                const double inv = 1.0 / ljj;                     // dpotf2 scales by 1/ajj
+                const double inv = rsqrt(d);                      // dpotf2 scales by 1/ajj
+                const double ljj = d * inv;
 #pragma unroll
                 for (int rr = 0; rr < RPL; ++rr) {
                     const int i = j + lane + 32 * rr;
@@ -353,31 +365,33 @@ __global__ void __launch_bounds__(128) gpr_warp_kernel(VoxelSolveArgs va, Proble
                 }
             }
             double b[NMAX];
+            if (VOXEL && kind == VX_KERNEL_SE && c > 0) {
+                // separable tables are zero on padding rows
 #pragma unroll
-            for (int i = 0; i < NMAX; ++i) {
-                double r = 0.0;
-                if (i < n) {
-                    if (c == 0) r = F[i];
-                    else if (!active) r = 0.0;
-                    else if (VOXEL && kind == VX_KERNEL_SE) r = EA[i * mm + ri] * EB[i * mm + si];
-                    else r = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], g0, g1));
+                for (int i = 0; i < NMAX; ++i) b[i] = active ? EA[i * mm + ri] * EB[i * mm + si] : 0.0;
+            } else {
+#pragma unroll
+                for (int i = 0; i < NMAX; ++i) {
+                    double r = 0.0;
+                    if (i < n && active) {
+                        if (c == 0) r = F[i];
+                        else r = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], g0, g1));
+                    }
+                    b[i] = r;
                 }
-                b[i] = r;
             }
             double ss = 0.0;
 #pragma unroll
             for (int i = 0; i < NMAX; ++i) {
-                if (i < n) {
+                if (i < n) {                                   // uniform: skips dead columns
                     const double w = b[i] * INV[i];
                     ss = fma(w, w, ss);
                     const double* Lc = L + i * LD;            // column i: L(r, i) at Lc[r]
 #pragma unroll
-                    for (int r = (i + 1) & ~1; r < NMAX; r += 2) {
-                        if (r < n) {
-                            const double2 l2 = *reinterpret_cast<const double2*>(Lc + r);
-                            b[r] = fma(-l2.x, w, b[r]);
-                            if (r + 1 < NMAX) b[r + 1] = fma(-l2.y, w, b[r + 1]);
-                        }
+                    for (int r = (i + 1) & ~1; r < NMAX; r += 2) {   // zero rows >= n
+                        const double2 l2 = *reinterpret_cast<const double2*>(Lc + r);
+                        b[r] = fma(-l2.x, w, b[r]);
+                        b[r + 1] = fma(-l2.y, w, b[r + 1]);
                     }
                     b[i] = w;                                  // (r == i above touched a dead value)
                 }
@@ -385,8 +399,7 @@ __global__ void __launch_bounds__(128) gpr_warp_kernel(VoxelSolveArgs va, Proble
             if (pass == 0) {
                 if (lane == 0) {
 #pragma unroll
-                    for (int i = 0; i < NMAX; ++i)
-                        if (i < n) NZ[i] = b[i];              // z = L^-1 f
+                    for (int i = 0; i < NMAX; ++i) NZ[i] = b[i];   // z = L^-1 f (0 on padding)
                 }
                 __syncwarp();
             }
@@ -394,8 +407,8 @@ __global__ void __launch_bounds__(128) gpr_warp_kernel(VoxelSolveArgs va, Proble
                 double mu0 = 0.0, mu1 = 0.0;
 #pragma unroll
                 for (int i = 0; i < NMAX; i += 2) {
-                    if (i < n) mu0 = fma(b[i], NZ[i], mu0);
-                    if (i + 1 < n) mu1 = fma(b[i + 1], NZ[i + 1], mu1);
+                    mu0 = fma(b[i], NZ[i], mu0);
+                    mu1 = fma(b[i + 1], NZ[i + 1], mu1);
                 }
                 const double mu = mu0 + mu1;
                 const double var = 1.0 - ss;
@@ -1816,7 +1829,8 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
     }
     switch (bucket) {
         case 0: return launch_warp<16, true>(a, none, a.num_items, a.M, mm, s);
-        case 1: return launch_warp<32, true>(a, none, a.num_items, a.M, mm, s);
+        case 1: return launch_warp<24, true>(a, none, a.num_items, a.M, mm, s);
+        case 5: return launch_warp<32, true>(a, none, a.num_items, a.M, mm, s);
         case 2:
             if (a.M + 1 <= 96) return launch_tile<8, 3, 4, true>(a, none, a.num_items, a.M, mm, s);
             return launch_warp<64, true>(a, none, a.num_items, a.M, mm, s);
@@ -1836,7 +1850,8 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
     if (count <= 0) return VX_OK;
     if (b.d_full == nullptr) {
         if (bucket == 0) return launch_warp<16, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 1) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 1) return launch_warp<24, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 5) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
         if (bucket == 2) return launch_tile<8, 3, 4, false>(none, pa, count, max_m, 1, s);
         if (bucket == 3) return launch_tile<16, 2, 6, false>(none, pa, count, max_m, 1, s);
         return launch_cta<false>(none, pa, count, max_n, max_m, 1, work, s);

@@ -40,7 +40,7 @@ struct VxMap {
     vx::DevBuf tkeys, tvals, tfirst, trank;
     // voxels
     int64_t num_voxels = 0, vcap = 0;
-    vx::DevBuf keys3, pkey, state, axis, raw_count, raw_off, raw_cap, pred_slot, has_pred;
+    vx::DevBuf keys3, pkey, state, axis, raw_count, raw_off, raw_cap, pred_slot, has_pred, last_first;
     // arena
     int64_t arena_top = 0, arena_cap = 0;
     vx::DevBuf axyz, argb;
@@ -77,9 +77,9 @@ enum {
     C_S,              // densify candidates
     C_MAXN,
     C_NEWSLOTS,
-    C_B0, C_B1, C_B2, C_B3, C_B4,   // bucket counts
-    C_F0, C_F1, C_F2, C_F3, C_F4,   // bucket fill cursors
-    C_O0, C_O1, C_O2, C_O3, C_O4,   // bucket bases
+    C_B0, C_B1, C_B2, C_B3, C_B4, C_B5,   // bucket counts
+    C_F0, C_F1, C_F2, C_F3, C_F4, C_F5,   // bucket fill cursors
+    C_O0, C_O1, C_O2, C_O3, C_O4, C_O5,   // bucket bases
     C_OK, C_DEGEN, C_CHOL, C_FIRST, C_CONV,
     C_COUNT
 };
@@ -211,6 +211,8 @@ struct CommitArgs {
     int32_t* pred_slot;
     uint8_t* has_pred;
     int32_t* frame_vids;
+    int32_t* last_first;
+    const uint64_t* tfirst;
     uint8_t* fb;
     int32_t* tbase;
     int64_t* treloc;
@@ -242,6 +244,7 @@ __global__ void k_touched_commit(CommitArgs a) {
         vid = a.tvals[slot];
     }
     a.frame_vids[r] = vid;
+    a.last_first[vid] = int32_t(uint32_t(a.tfirst[slot]));   // first point of this frame
     a.fb[r] = a.state[vid];
     a.tbase[r] = a.raw_count[vid];
     a.treloc[r] = -1;
@@ -420,6 +423,7 @@ static int ensure_voxels(VxMap* m, int64_t need, cudaStream_t s) {
     VX_TRY(grow_array<int32_t>(m->raw_cap, n, cap, s));
     VX_TRY(grow_array<int32_t>(m->pred_slot, n, cap, s));
     VX_TRY(grow_array<uint8_t>(m->has_pred, n, cap, s));
+    VX_TRY(grow_array<int32_t>(m->last_first, n, cap, s));
     m->vcap = cap;
     return VX_OK;
 }
@@ -612,7 +616,8 @@ static int map_store_frame_impl(VxMap* m, const double* xyz, const double* rgb, 
                   m->keys3.as<int64_t>(), m->pkey.as<uint64_t>(), m->state.as<uint8_t>(),
                   m->axis.as<int8_t>(), m->raw_count.as<int32_t>(), m->raw_off.as<int64_t>(),
                   m->raw_cap.as<int32_t>(), m->pred_slot.as<int32_t>(), m->has_pred.as<uint8_t>(),
-                  m->frame_vids.as<int32_t>(), m->fb.as<uint8_t>(), m->tbase.as<int32_t>(),
+                  m->frame_vids.as<int32_t>(), m->last_first.as<int32_t>(),
+                  m->tfirst.as<uint64_t>(), m->fb.as<uint8_t>(), m->tbase.as<int32_t>(),
                   m->treloc.as<int64_t>()};
     k_touched_commit<<<nblk(U), 256, 0, s>>>(ca);
     count_launch();
@@ -854,7 +859,7 @@ VxMap* map_new(const VxMapConfig& cfg, int* rc) {
 }
 
 void map_delete(VxMap* m) {
-    DevBuf* bufs[] = {&m->tkeys, &m->tvals, &m->tfirst, &m->trank, &m->keys3, &m->pkey, &m->state,
+    DevBuf* bufs[] = {&m->tkeys, &m->tvals, &m->tfirst, &m->trank, &m->keys3, &m->pkey, &m->state, &m->last_first,
                       &m->axis, &m->raw_count, &m->raw_off, &m->raw_cap, &m->pred_slot, &m->has_pred,
                       &m->axyz, &m->argb, &m->pxyz, &m->prgb, &m->pvar, &m->pslot, &m->flags,
                       &m->fscan, &m->prank, &m->pidx, &m->prank2, &m->pidx2, &m->tslot, &m->tcnt,
@@ -878,6 +883,7 @@ void map_fill_view(VxMap* m, VxMapView* v) {
     v->raw_offset = m->raw_off.as<int64_t>();
     v->pred_slot = m->pred_slot.as<int32_t>();
     v->has_pred = m->has_pred.as<uint8_t>();
+    v->last_first = m->last_first.as<int32_t>();
     v->raw_xyz = m->axyz.as<double>();
     v->raw_rgb = m->argb.as<double>();
     v->pred_points = m->M;

@@ -387,3 +387,37 @@ def test_eigen_rotation_extension_reconstructs_phi():
         if ev.min() > 1e-8:   # no scale floor active
             np.testing.assert_allclose(R @ s2 @ R.T, phi, atol=1e-12)
         assert abs(np.linalg.norm(q) - 1) < 1e-12
+
+
+def test_hash_sharded_maps_reassemble_single_gpu_result():
+    """Two shards (rank 0/1 of world 2) on one device == the unsharded map.
+
+    Each shard keeps mix64(key) % 2 == rank; their records merged by the
+    order key (frame, first point index) equal the single-GPU records exactly.
+    """
+    import torch
+    from paper_2410_17084_b200 import sharding
+    sc = scenes.OutdoorScene.make(0)
+    config = vx.PipelineConfig(voxel_size=0.5)
+    full = vx.MappingEngine(config)
+    shards = [sharding.ShardedEngine(config, r, 2) for r in range(2)]
+    for fr in range(2):
+        pos, col = scenes.config1_scan(seed=0, frame=fr, rays=20000)
+        pin = scenes.camera_for(fr, 160, 120, 100.0)
+        img = scenes.render_image(sc, pin)
+        cam = vx.Camera(pin.fx, pin.fy, pin.cx, pin.cy, pin.width, pin.height, pin.R, pin.t)
+        full.ingest(pos, col, cam, img)
+        for sh in shards:
+            sh.ingest(pos, col, cam, img)
+    recs = [sh.engine.gaussians_device() for sh in shards]
+    order = torch.cat([torch.cat(sh.orders) for sh in shards])
+    perm = torch.sort(order, stable=True).indices
+    ref = full.gaussians_device()
+    for k in ref:
+        merged = torch.cat([r[k] for r in recs]).index_select(0, perm)
+        assert torch.equal(merged, ref[k]), k
+    own = sharding.owner_of(ref["source_key"].cpu().numpy(), 2)
+    for r in range(2):
+        np.testing.assert_array_equal(np.unique(sharding.owner_of(
+            recs[r]["source_key"].cpu().numpy(), 2)), [r])
+    assert len(own) == sum(len(r["opacity"]) for r in recs)
