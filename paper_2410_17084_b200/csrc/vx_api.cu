@@ -281,7 +281,7 @@ int vx_voxel_keys(const double* d_xyz, int64_t n, double voxel_size, int64_t* d_
     std::lock_guard<std::mutex> lk(g_scratch_mu);
     Scratch& sc = scratch();
     VX_TRY(sc.a.reserve(sizeof(int), s));
-    if (!sc.host) VX_CUDA(cudaMallocHost(&sc.host, 64));
+    if (!sc.host) VX_CUDA(cudaMallocHost(&sc.host, 256));
     VX_CUDA(cudaMemsetAsync(sc.a.ptr, 0, sizeof(int), s));
     k_voxel_keys<<<unsigned((n * 3 + 255) / 256), 256, 0, s>>>(d_xyz, n, voxel_size, d_keys,
                                                                sc.a.as<int>());
@@ -354,11 +354,11 @@ int vx_gpr_solve_batch(const VxGprBatch* b, void* stream) {
     cudaStream_t s = as_stream(stream);
     std::lock_guard<std::mutex> lk(g_scratch_mu);
     Scratch& sc = scratch();
-    if (!sc.host) VX_CUDA(cudaMallocHost(&sc.host, 64));
+    if (!sc.host) VX_CUDA(cudaMallocHost(&sc.host, 256));
     VX_TRY(sc.a.reserve(size_t(P) * 4, s));
-    VX_TRY(sc.b.reserve(64, s));
+    VX_TRY(sc.b.reserve(256, s));
     int* cnt = sc.b.as<int>();
-    VX_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
+    VX_CUDA(cudaMemsetAsync(cnt, 0, 256, s));   // [0,16) counts, [16,32) fill, [32,48) bases
     const unsigned g = unsigned((P + 255) / 256);
     k_problem_count<<<g, 256, 0, s>>>(b->d_x_off, P, cnt);
     count_launch();
@@ -370,11 +370,11 @@ int vx_gpr_solve_batch(const VxGprBatch* b, void* stream) {
     for (int k = 0; k < NUM_BUCKETS; ++k) {
         counts[k] = sc.host[k];
         offs[k] = acc;
-        sc.host[8 + k] = int(acc);
+        sc.host[32 + k] = int(acc);
         acc += counts[k];
     }
-    VX_CUDA(cudaMemcpyAsync(cnt + 8, sc.host + 8, NUM_BUCKETS * sizeof(int), cudaMemcpyHostToDevice, s));
-    k_problem_buckets<<<g, 256, 0, s>>>(b->d_x_off, P, sc.a.as<int32_t>(), cnt + 4, cnt + 8);
+    VX_CUDA(cudaMemcpyAsync(cnt + 32, sc.host + 32, NUM_BUCKETS * sizeof(int), cudaMemcpyHostToDevice, s));
+    k_problem_buckets<<<g, 256, 0, s>>>(b->d_x_off, P, sc.a.as<int32_t>(), cnt + 16, cnt + 32);
     count_launch();
     VX_CHECK_LAUNCH();
     for (int k = NUM_BUCKETS - 1; k >= 0; --k) {

@@ -219,6 +219,29 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// Warp-aggregated counters: lanes hitting the same counter share one atomic
+// (the densify bookkeeping kernels otherwise serialise ~1M same-address atomics).
+__device__ __forceinline__ unsigned long long agg_add(unsigned long long* ctr, int key,
+                                                      unsigned long long v = 1) {
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, key);
+    const int leader = __ffs(peers) - 1;
+    const int lane = threadIdx.x & 31;
+    // every lane adds v, so the warp total for this key is v * popc(peers)
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(ctr + key, v * (unsigned long long)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    return base + v * (unsigned long long)__popc(peers & lt);
+}
+
+__device__ __forceinline__ void agg_max(unsigned long long* ctr, unsigned v) {
+    const unsigned act = __activemask();
+    const unsigned mx = __reduce_max_sync(act, v);
+    if ((threadIdx.x & 31) == __ffs(act) - 1) atomicMax(ctr, (unsigned long long)mx);
+}
+
 // named barrier for a team of `nthreads` threads (multiple of 32).  The
 // non-.aligned form: callers keep every barrier on a team-uniform path, but
 // bar.sync (== barrier.sync.aligned) would make any divergence undefined.

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(128) k_pca_prepass(VoxelSolveArgs a, int S, lo
     const double sum = np_pairwise_sum(
         [&](int i) { return train_point(a, i, cnt, off, slot)[ax]; }, n);
     a.cand_meanf[s] = xdiv(sum, double(n));                    // f.mean() (gpr.py:291)
-    atomicAdd(reinterpret_cast<unsigned long long*>(buckets + bucket_of(n)), 1ull);
+    agg_add(reinterpret_cast<unsigned long long*>(buckets), bucket_of(n));
 }
 
 __global__ void k_bucket_items(const int32_t* cand_n, const int8_t* cand_axis, int S, int32_t* items,
@@ -132,7 +132,7 @@ __global__ void k_bucket_items(const int32_t* cand_n, const int8_t* cand_axis, i
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= S || cand_axis[s] < 0) return;
     const int b = bucket_of(cand_n[s]);
-    const long long pos = atomicAdd(reinterpret_cast<unsigned long long*>(fill + b), 1ull);
+    const long long pos = agg_add(reinterpret_cast<unsigned long long*>(fill), b);
     items[base[b] + pos] = int32_t(s);
 }
 

@@ -125,10 +125,7 @@ __global__ void k_hash_points(const double* __restrict__ xyz, int64_t n, double 
         if (cur == EMPTY_KEY) {
             uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(tkeys + h),
                                       (unsigned long long)EMPTY_KEY, (unsigned long long)pk);
-            if (prev == EMPTY_KEY) {
-                atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_INSERTED), 1ull);
-                break;
-            }
+            if (prev == EMPTY_KEY) break;
             if (prev == pk) break;
         }
         h = (h + 1) & uint64_t(tmask);
@@ -301,7 +298,7 @@ __global__ void k_touched_finish(const int32_t* frame_vids, const int32_t* tbase
     if (st == VX_UNREADY && c >= tau) {       // voxel_map.py:339-340
         st = VX_READY;
         state[vid] = st;
-        atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_READY), 1ull);
+        agg_add(reinterpret_cast<unsigned long long*>(ctr), C_READY);
     }
     fa[r] = st;
 }
@@ -344,9 +341,9 @@ __global__ void k_dens_list(const int32_t* frame_vids, const int32_t* cflag, con
     cand_voxel[s] = vid;
     cand_n[s] = n;
     cand_status[s] = 255;
-    atomicMax(reinterpret_cast<unsigned long long*>(ctr + C_MAXN), (unsigned long long)n);
+    agg_max(reinterpret_cast<unsigned long long*>(ctr + C_MAXN), unsigned(n));
     if (pred_slot[vid] < 0) {
-        const long long k = atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_NEWSLOTS), 1ull);
+        const long long k = agg_add(reinterpret_cast<unsigned long long*>(ctr), C_NEWSLOTS);
         pred_slot[vid] = int32_t(slot_base + k);
     }
 }
@@ -357,15 +354,12 @@ __global__ void k_dens_finish(const uint8_t* status, const uint8_t* before, cons
     if (s >= S) return;
     const uint8_t st = status[s];
     okflag[s] = st == VX_ST_OK ? 1 : 0;
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(ctr);
     if (st == VX_ST_OK) {
-        if (before[s] == VX_READY)
-            atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_FIRST), 1ull);
-        if (after[s] == VX_CONVERGED)
-            atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_CONV), 1ull);
-    } else if (st == VX_ST_DEGENERATE) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_DEGEN), 1ull);
+        if (before[s] == VX_READY) agg_add(c, C_FIRST);
+        if (after[s] == VX_CONVERGED) agg_add(c, C_CONV);
     } else {
-        atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_CHOL), 1ull);
+        agg_add(c, st == VX_ST_DEGENERATE ? C_DEGEN : C_CHOL);
     }
 }
 
