@@ -1834,8 +1834,11 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 2:
             if (a.M + 1 <= 96) return launch_tile<8, 3, 4, true>(a, none, a.num_items, a.M, mm, s);
             return launch_warp<64, true>(a, none, a.num_items, a.M, mm, s);
+        case 6:
+            if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
+            return launch_cta<true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
         case 3:
-            if (a.M + 1 <= 96) return launch_tile<16, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
+            if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
         default: return launch_cta<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
     }
@@ -1853,7 +1856,8 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
         if (bucket == 1) return launch_warp<24, false>(none, pa, count, max_m, 1, s);
         if (bucket == 5) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
         if (bucket == 2) return launch_tile<8, 3, 4, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 3) return launch_tile<16, 2, 6, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 6) return launch_tile<16, 1, 12, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 3) return launch_tile<16, 1, 12, false>(none, pa, count, max_m, 1, s);
         return launch_cta<false>(none, pa, count, max_n, max_m, 1, work, s);
     }
     return launch_generic<false>(none, pa, count, max_n, max_m, work, s);

@@ -77,9 +77,9 @@ enum {
     C_S,              // densify candidates
     C_MAXN,
     C_NEWSLOTS,
-    C_B0, C_B1, C_B2, C_B3, C_B4, C_B5,   // bucket counts
-    C_F0, C_F1, C_F2, C_F3, C_F4, C_F5,   // bucket fill cursors
-    C_O0, C_O1, C_O2, C_O3, C_O4, C_O5,   // bucket bases
+    C_B0, C_B1, C_B2, C_B3, C_B4, C_B5, C_B6,   // bucket counts
+    C_F0, C_F1, C_F2, C_F3, C_F4, C_F5, C_F6,   // bucket fill cursors
+    C_O0, C_O1, C_O2, C_O3, C_O4, C_O5, C_O6,   // bucket bases
     C_OK, C_DEGEN, C_CHOL, C_FIRST, C_CONV,
     C_COUNT
 };
@@ -116,7 +116,7 @@ __global__ void k_hash_points(const double* __restrict__ xyz, int64_t n, double 
     if (world > 1 && shard_of(pk, world) != uint32_t(rank)) return;
     uint64_t h = mix64(pk) & uint64_t(tmask);
     for (int64_t probe = 0;; ++probe) {
-        if (probe > tmask) {
+        if (probe > 256 || probe > tmask) {      // table too full: host grows + retries
             atomicOr(reinterpret_cast<unsigned long long*>(ctr + C_ERR), 4ull);
             return;
         }
@@ -513,7 +513,11 @@ static int map_store_frame_impl(VxMap* m, const double* xyz, const double* rgb, 
     VX_TRY(m->prank2.reserve(n * 4, s));
     VX_TRY(m->pidx2.reserve(n * 4, s));
     // table: keep load <= 1/2 even if every point opens a voxel
-    int64_t want = 2 * (m->num_voxels + n) + 1024;
+    // Table sized for load <= 1/2 with an estimate of the frame's new voxels
+    // (points / 8): a small table stays (mostly) L2-resident.  If the frame opens more
+    // voxels, the insert kernel flags a long probe and the frame is re-hashed
+    // into a 4x table (the retry only re-inserts the existing voxels).
+    int64_t want = 2 * (m->num_voxels + std::max<int64_t>(n / 8, 4096));
     if (m->tcap < want) VX_TRY(rebuild_table(m, want, s));
 
     const double vs = m->cfg.voxel_size;
@@ -541,7 +545,7 @@ static int map_store_frame_impl(VxMap* m, const double* xyz, const double* rgb, 
             set_error("voxel key outside the supported lattice |k| < 2^20 (voxel_size %g)", vs);
             return VX_E_RANGE;
         }
-        if ((err & 4) && attempt == 0) {
+        if ((err & 4) && attempt < 6) {
             VX_TRY(rebuild_table(m, m->tcap * 4, s));
             continue;
         }

@@ -97,6 +97,65 @@ class MappingEngine:
         rep.duration_s = time.perf_counter() - t0
         return rep
 
+    def ingest_stream(self, frames, reset_each: bool = False) -> list:
+        """Ingest a sequence of host frames with H2D double-buffering.
+
+        `frames` yields (positions, colors, camera, image) with positions /
+        colors as (n, 3) float64 host tensors (pinned for true overlap) and
+        image an (H, W, 3) float64 host tensor or None.  The copy of frame k+1
+        runs on a side stream while frame k is processed, so a steady stream
+        costs max(H2D, device work) per frame instead of their sum.
+        """
+        import torch
+        dev = N.device()
+        compute = torch.cuda.current_stream()
+        if getattr(self, "_copier", None) is None:
+            # persistent side stream + double buffers (allocated once, reused)
+            self._copier = torch.cuda.Stream(device=dev)
+            self._bufs = [dict(), dict()]
+            self._free = [None, None]
+        copier, bufs, free = self._copier, self._bufs, self._free
+        reports = []
+        it = iter(frames)
+
+        def issue(frame, slot):
+            pos, col, cam, img = frame
+            with torch.cuda.stream(copier):
+                if free[slot] is not None:
+                    copier.wait_event(free[slot])
+                b = bufs[slot]
+                for name, t in (("xyz", pos), ("rgb", col), ("img", img)):
+                    if t is None:
+                        b[name] = None
+                        continue
+                    t = t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t))
+                    cur = b.get(name)
+                    if cur is None or cur.shape != t.shape:
+                        cur = torch.empty(t.shape, dtype=t.dtype, device=dev)
+                        b[name] = cur
+                    if cur.numel():
+                        cur.copy_(t, non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(copier)
+            return (b["xyz"], b["rgb"], int(pos.shape[0]), cam, b["img"], ready)
+
+        nxt = next(it, None)
+        pending = issue(nxt, 0) if nxt is not None else None
+        k = 0
+        while pending is not None:
+            dx, dc, n, cam, di, ready = pending
+            nxt = next(it, None)
+            pending = issue(nxt, (k + 1) & 1) if nxt is not None else None
+            compute.wait_event(ready)
+            if reset_each:
+                self.reset()
+            reports.append(self.ingest_device(dx, dc, n, cam, di))
+            done = torch.cuda.Event()
+            done.record(compute)
+            free[k & 1] = done
+            k += 1
+        return reports
+
     def ingest_device(self, d_xyz, d_rgb, n: int, camera=None, d_image=None) -> IngestReport:
         t0 = time.perf_counter()
         cfg = self.config
