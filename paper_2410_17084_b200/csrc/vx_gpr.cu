@@ -1404,11 +1404,12 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                     }
                     __syncthreads();
                 }
-                // (b) every warp factors the 8x8 diagonal block redundantly (lane r
-                // holds row r); identical inputs give identical outputs, so the
-                // duplicate shared-memory stores are benign and no barrier separates
-                // the factorisation from the rows below
-                {
+                // (b) the warps that solve rows below this block (and warp 0, which
+                // publishes INV / LDG / the pivot flag) factor the 8x8 diagonal block
+                // redundantly (lane r holds row r).  Identical inputs give identical
+                // outputs, so the duplicate shared-memory stores are benign and no
+                // barrier separates the factorisation from the rows below.
+                if (warp == 0 || warp * 32 < n8 - j0 - 8) {
                     double d[8];
                     const int r = lane & 7;
 #pragma unroll
@@ -1418,8 +1419,8 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                     for (int c = 0; c < 8; ++c) {
                         const double piv = __shfl_sync(FULL, d[c], c);
                         if (!(piv > 0.0)) okw = false;
-                        const double lcc = sqrt(piv);
-                        const double inv = 1.0 / lcc;
+                        const double inv = rsqrt(piv);          // dpotf2 scales by 1/ajj
+                        const double lcc = piv * inv;
                         if (r == c) d[c] = lcc;
                         else if (r > c) d[c] = d[c] * inv;
 #pragma unroll
@@ -1433,11 +1434,8 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
 #pragma unroll                                        // still be reading the block in L
                         for (int k = 0; k < 8; ++k) LDG[(j0 + r) * 8 + k] = (k <= r) ? d[k] : 0.0;
                     }
+                    if (warp == 0 && lane == 0) smem[lay.FLAG] = okw ? 1.0 : 0.0;
                     __syncwarp();
-                    if (!okw) {                       // uniform across the CTA
-                        ok = false;
-                        break;
-                    }
                 }
                 // (c) rows below the block: L(i, J) = A(i, J) L_JJ^-T
                 for (int i = j0 + 8 + tid; i < n8; i += NT) {
@@ -1453,6 +1451,10 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                     for (int c = 0; c < 8; ++c) L[(j0 + c) * LDL + i] = v[c];
                 }
                 __syncthreads();
+                if (smem[lay.FLAG] == 0.0) {          // pivot <= 0 or NaN: uniform exit
+                    ok = false;
+                    break;
+                }
             }
             __syncthreads();
         }
@@ -1744,7 +1746,7 @@ static int launch_cta(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_i
         const int cap = sm_count() * per_sm;
         if (blocks > cap) blocks = cap;
     } else {
-        int cap = sm_count() * 2;
+        int cap = sm_count() * 6;      // latency-bound on the L2 workspace: oversubscribe
         const int64_t max_blocks = (int64_t(4) << 30) / int64_t(bytes);
         if (cap > max_blocks) cap = int(max_blocks > 0 ? max_blocks : 1);
         if (blocks > cap) blocks = cap;
