@@ -173,7 +173,7 @@ __device__ __forceinline__ void tri_decode(int idx, int* i, int* j) {
 }
 
 template <int NMAX, bool VOXEL>
-__global__ void __launch_bounds__(128) gpr_warp_kernel(VoxelSolveArgs va, ProblemArgs pa, int mmax,
+__global__ void __launch_bounds__(128, NMAX <= 16 ? 5 : (NMAX <= 24 ? 4 : (NMAX <= 32 ? 3 : 1))) gpr_warp_kernel(VoxelSolveArgs va, ProblemArgs pa, int mmax,
                                                        int mm) {
     extern __shared__ __align__(16) double smem[];
     constexpr int LD = NMAX;
