@@ -296,10 +296,23 @@ def run_gpu(args, rank, world, local_rank):
     if top in bucket:
         flops = float(gpr_flops(bucket[top]).sum()) * args.steps
         achieved = flops / (top_ms / 1e3) / 1e12
+        # DRAM traffic per launch: bytes/voxel of this kernel from the committed
+        # ncu --set full capture (tools/ncu_traffic.py) x voxels in this launch
+        traffic, tnote = None, "no committed ncu capture for this kernel"
+        tfile = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles"))
+                       if f.endswith("_traffic.json")) if os.path.isdir(
+                           os.path.join(ROOT, "profiles")) else []
+        if tfile:
+            tj = json.load(open(os.path.join(ROOT, "profiles", tfile[-1])))
+            if top in tj:
+                traffic = tj[top]["bytes_per_voxel"] * len(bucket[top])
+                tnote = (f"profiles/{tfile[-1]}: {tj[top]['bytes_per_voxel']:.0f} B/voxel measured "
+                         f"(dram read+write) x {len(bucket[top])} voxels; algorithmic "
+                         f"{56 * (float(bucket[top].mean()) + NSTAR):.0f} B/voxel")
         roof = {"kernel": top, "bound": "fp64", "achieved": achieved, "peak": peak64,
                 "unit": "TFLOP/s", "frac": achieved / peak64,
                 "peak_source": "measured in-run DFMA microbenchmark (vx_fp64_peak)",
-                "traffic": None, "launch_ms": top_ms / top_n,
+                "traffic": traffic, "traffic_note": tnote, "launch_ms": top_ms / top_n,
                 "share_of_step": top_ms / ms}
     else:
         # hashing / splat are HBM-bound: algorithmic bytes per point = 104

@@ -141,7 +141,7 @@ __global__ void k_bucket_items(const int32_t* cand_n, const int8_t* cand_axis, i
 // ---------------------------------------------------------------------------
 // per-warp shared-memory slice (doubles), LD = NMAX (even: 16-byte columns)
 struct WarpLayout {
-    int X, F, NZ, L, INV, EA, EB, MU, VAR, COL, BI, total;
+    int X, F, NZ, L, INV, EA, EB, MU, VAR, COL, BI, GC, total;
     __host__ __device__ WarpLayout(int NMAX, int mm, int m, bool voxel) {
         int o = 0;
         X = o; o += 2 * NMAX;
@@ -150,7 +150,7 @@ struct WarpLayout {
         L = o; o += NMAX * NMAX;
         INV = o; o += NMAX;
         EA = o; EB = o;
-        MU = VAR = COL = BI = o;
+        MU = VAR = COL = BI = GC = o;
         if (voxel) {
             EA = o; o += NMAX * mm;
             EB = o; o += NMAX * mm;
@@ -158,6 +158,7 @@ struct WarpLayout {
             VAR = o; o += m;
             COL = o; o += 3 * m;
             BI = o; o += (m + 1) / 2;  // int32 pairs
+            GC = o; o += 2 * mm;       // grid coordinates c0[mm], c1[mm]
         }
         total = (o + 1) & ~1;
     }
@@ -223,19 +224,25 @@ __global__ void __launch_bounds__(128, NMAX <= 16 ? 5 : (NMAX <= 24 ? 4 : (NMAX 
             lo1 = xmul(double(va.keys[int64_t(vid) * 3 + pb_]), va.voxel_size);
             sp0 = xsub(xadd(lo0, va.voxel_size), lo0);
             sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
+            // grid coordinates c_r = lo + ((r + 0.5) * (hi - lo)) / m, once per voxel
+            if (lane < 2 * mm) {
+                const int which = lane >= mm, r = lane - which * mm;
+                base[lay.GC + lane] = xadd(which ? lo1 : lo0,
+                                           xdiv(xmul(double(r) + 0.5, which ? sp1 : sp0), double(mm)));
+            }
             __syncwarp();
+            const double* GC = base + lay.GC;
             if (kind == VX_KERNEL_SE) {
                 double* EA = base + lay.EA;
                 double* EB = base + lay.EB;
                 // lane = (table, training row); rows >= n get zeros (padding)
                 for (int e = lane; e < 2 * NMAX; e += 32) {
                     const int which = e / NMAX, i = e - which * NMAX;
-                    const double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
                     double* T = (which ? EB : EA) + i * mm;
                     if (i < n) {
                         const double xi = X[2 * i + which];
                         for (int r = 0; r < mm; ++r) {
-                            const double g = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
+                            const double g = GC[which * mm + r];
                             const double d = xsub(xi, g);
                             T[r] = exp(xmul(-lam, xmul(d, d)));
                         }
@@ -357,8 +364,8 @@ __global__ void __launch_bounds__(128, NMAX <= 16 ? 5 : (NMAX <= 24 ? 4 : (NMAX 
                     const int fr = rem2 / nr, fc = rem2 - fr * nr;
                     ri = sr * nr + fr;
                     si = sc * nr + fc;
-                    g0 = xadd(lo0, xdiv(xmul(double(ri) + 0.5, sp0), double(mm)));
-                    g1 = xadd(lo1, xdiv(xmul(double(si) + 0.5, sp1), double(mm)));
+                    g0 = base[lay.GC + ri];
+                    g1 = base[lay.GC + mm + si];
                 } else {
                     g0 = pa.xs[(qo + q) * 2];
                     g1 = pa.xs[(qo + q) * 2 + 1];
@@ -456,8 +463,8 @@ __global__ void __launch_bounds__(128, NMAX <= 16 ? 5 : (NMAX <= 24 ? 4 : (NMAX 
                 const int fr = rem2 / nr, fc = rem2 - fr * nr;
                 double pos[3];
                 pos[axis] = base[lay.MU + q];
-                pos[pa_] = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
-                pos[pb_] = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
+                pos[pa_] = base[lay.GC + sr * nr + fr];
+                pos[pb_] = base[lay.GC + mm + sc * nr + fc];
                 oxyz[q * 3] = pos[0];
                 oxyz[q * 3 + 1] = pos[1];
                 oxyz[q * 3 + 2] = pos[2];

@@ -1,0 +1,49 @@
+"""DRAM traffic per solved voxel of each GPR kernel, from one `ncu --set full`
+capture of `bench.py --voxels V --steps 1 --warmup 1` (first densify only).
+
+    python tools/ncu_traffic.py <report.ncu-rep> <V> > profiles/<round>_traffic.json
+
+The bucket voxel counts are recomputed from the same seeded workload, so the
+bytes/voxel figure can be scaled to any launch of the same kernel (bench.py
+reports `roofline.traffic` that way).
+"""
+import csv
+import json
+import os
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+import bench  # noqa: E402
+
+rep, V = sys.argv[1], int(sys.argv[2])
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+hdr = rows[0]
+col = {h: i for i, h in enumerate(hdr)}
+_, _, counts, *_ = bench.make_workload(V, 0)
+sol = counts[counts >= bench.TAU]
+# launch order within one densify is bucket id 6, 5, 4, 3, 2, 1, 0 (largest first)
+buckets = [("gpr_tile_kernel<16, 1, 12", (64, 96), "gpr_tile96"),
+           ("gpr_warp_kernel<32", (24, 32), "gpr_warp32"),
+           ("gpr_cta_kernel", (128, 10 ** 9), "gpr_cta_large"),
+           ("gpr_tile_kernel<16, 1, 12", (96, 128), "gpr_tile128"),
+           ("gpr_tile_kernel<8", (32, 64), "gpr_tile64"),
+           ("gpr_warp_kernel<24", (16, 24), "gpr_warp24"),
+           ("gpr_warp_kernel<16", (0, 16), "gpr_warp16")]
+res = {}
+for r in rows[2:]:
+    name = r[col["Kernel Name"]]
+    rd = float(r[col["dram__bytes_read.sum"]])
+    wr = float(r[col["dram__bytes_write.sum"]])
+    unit = rows[1][col["dram__bytes_read.sum"]]
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    tot = (rd + wr) * mult
+    for key, (lo, hi), label in buckets:
+        if key in name and label not in res:
+            n = int(((sol > lo) & (sol <= hi)).sum())
+            res[label] = {"dram_bytes": tot, "voxels": n, "bytes_per_voxel": tot / max(n, 1),
+                          "kernel": name}
+            break
+print(json.dumps(res, indent=1))
