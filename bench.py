@@ -292,7 +292,8 @@ def run_gpu(args, rank, world, local_rank):
               "gpr_warp32": sol[(sol > 24) & (sol <= 32)],
               "gpr_tile64": sol[(sol > 32) & (sol <= 64)],
               "gpr_tile96": sol[(sol > 64) & (sol <= 96)],
-              "gpr_tile128": sol[(sol > 96) & (sol <= 128)], "gpr_cta_large": sol[sol > 128]}
+              "gpr_tile128": sol[(sol > 96) & (sol <= 128)],
+              "gpr_cta160": sol[(sol > 128) & (sol <= 160)], "gpr_cta_large": sol[sol > 160]}
     if top in bucket:
         flops = float(gpr_flops(bucket[top]).sum()) * args.steps
         achieved = flops / (top_ms / 1e3) / 1e12

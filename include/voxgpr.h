@@ -309,8 +309,8 @@ int vx_fp64_peak(double* tflops, void* stream);
 /* CUDA-event timers around the library's stages, recorded on the launching
  * stream: 0 store_frame (hashing), 1-2 GPR warp kernels n<=16/24,
  * 3-4 GPR DMMA tile kernels n<=64/128, 5 GPR CTA kernel n>128, 6 warp kernel
- * n<=32, 7 DMMA tile kernel n<=96, 8 Gaussian init, 9 whole densify,
- * 10 PCA prepass.  vx_profile(1) resets
+ * n<=32, 7 DMMA tile kernel n<=96, 8 CTA kernel 128<n<=160, 9 Gaussian
+ * init, 10 whole densify, 11 PCA prepass.  vx_profile(1) resets
  * and enables; vx_profile_read fills total ms and launch counts per stage
  * and returns the number of stages. */
 int vx_profile(int enable);

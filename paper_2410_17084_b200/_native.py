@@ -260,7 +260,7 @@ def splat_struct(n_s, n_r, weight_floor, scale_floor, opacity, rotation="identit
 
 
 PROFILE_STAGES = ("hash", "gpr_warp16", "gpr_warp24", "gpr_tile64", "gpr_tile128", "gpr_cta_large",
-                  "gpr_warp32", "gpr_tile96", "splat", "densify", "pca")
+                  "gpr_warp32", "gpr_tile96", "gpr_cta160", "splat", "densify", "pca")
 
 
 def profile(enable: bool) -> None:

@@ -1245,12 +1245,26 @@ __device__ __forceinline__ void dmma_acc(double& c0, double& c1, double a, doubl
         : "d"(a), "d"(b));
 }
 
+// Packed block-column storage of the lower triangle: block column kb (columns
+// 8kb..8kb+7) holds rows 8kb..n8-1 column-major with leading dimension
+// ldb = rows + (4 or 12) so that ldb = 4 (mod 16) doubles and the four
+// columns of a DMMA fragment load land on disjoint bank pairs.
+__host__ __device__ inline int tile_ldb(int n8, int kb) {
+    const int rows = n8 - 8 * kb;
+    return rows + ((rows & 15) ? 12 : 4);
+}
+__host__ __device__ inline int tile_packed(int n8) {
+    int t = 0;
+    for (int kb = 0; kb < n8 / 8; ++kb) t += 8 * tile_ldb(n8, kb);
+    return t;
+}
+
 struct TileLayout {
-    int L, LINV, LDG, X, F, NZ, INV, Z, EA, EB, MU, VAR, BI, COL, FLAG, total, ld;
+    int L, CO, LINV, LDG, X, F, NZ, INV, Z, EA, EB, MU, VAR, BI, COL, FLAG, total;
     __host__ __device__ TileLayout(int N8, int mm, int mcols, int mmax, bool voxel) {
-        ld = N8 + 4;
         int o = 0;
-        L = o; o += N8 * ld;
+        L = o; o += tile_packed(N8);
+        CO = o; o += N8 / 2 + 1;        // int32 column offsets: L(i, j) = L[CO[j] + i]
         LINV = o; o += N8 * 8;          // inverses of the 8x8 diagonal blocks, row-major
         LDG = o; o += N8 * 8;           // factored 8x8 diagonal blocks, row-major
         X = o; o += 2 * N8;
@@ -1273,14 +1287,13 @@ struct TileLayout {
 };
 
 template <int NRB, int CTW, int NW, bool VOXEL>
-__global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
+__global__ void __launch_bounds__(NW * 32, 1) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
                                                            int mmax, int mm) {
     extern __shared__ __align__(16) double smem[];
     constexpr int N8 = NRB * 8;
     constexpr int NT = NW * 32;
     constexpr int PCOLS = NW * CTW * 8;             // right-hand sides per pass
     const TileLayout lay(N8, mm, PCOLS, mmax, VOXEL);
-    const int LDL = lay.ld;
     double* L = smem + lay.L;
     double* X = smem + lay.X;
     double* F = smem + lay.F;
@@ -1288,6 +1301,7 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
     double* INV = smem + lay.INV;
     double* Z = smem + lay.Z;
     double* LDG = smem + lay.LDG;
+    int* CO = reinterpret_cast<int*>(smem + lay.CO);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, tig = lane & 3;
     const int num_items = VOXEL ? va.num_items : pa.num_items;
@@ -1367,6 +1381,12 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
         }
         const int nrb = (n + 7) >> 3;
         const int n8 = nrb * 8;
+        for (int j = tid; j < n8; j += NT) {
+            const int kb = j >> 3;
+            int o = 0;
+            for (int t = 0; t < kb; ++t) o += 8 * tile_ldb(n8, t);
+            CO[j] = o + (j & 7) * tile_ldb(n8, kb) - 8 * kb;
+        }
         __syncthreads();
 
         // ---- A (identity-padded), panel Cholesky with DMMA updates, one retry
@@ -1389,7 +1409,7 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                 } else {
                     v = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
                 }
-                L[j * LDL + i] = v;
+                L[CO[j] + i] = v;
             }
             __syncthreads();
             ok = true;
@@ -1399,15 +1419,15 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                 if (j0 > 0) {
                     for (int t = kb + warp; t < nrb; t += NW) {
                         const int rb = t * 8;
-                        double c0 = L[(j0 + 2 * tig) * LDL + rb + g];
-                        double c1 = L[(j0 + 2 * tig + 1) * LDL + rb + g];
+                        double c0 = L[CO[j0 + 2 * tig] + rb + g];
+                        double c1 = L[CO[j0 + 2 * tig + 1] + rb + g];
                         for (int k4 = 0; k4 < j0; k4 += 4) {
-                            const double a = -L[(k4 + tig) * LDL + rb + g];
-                            const double b = L[(k4 + tig) * LDL + j0 + g];
+                            const double a = -L[CO[k4 + tig] + rb + g];
+                            const double b = L[CO[k4 + tig] + j0 + g];
                             dmma_acc(c0, c1, a, b);
                         }
-                        L[(j0 + 2 * tig) * LDL + rb + g] = c0;
-                        L[(j0 + 2 * tig + 1) * LDL + rb + g] = c1;
+                        L[CO[j0 + 2 * tig] + rb + g] = c0;
+                        L[CO[j0 + 2 * tig + 1] + rb + g] = c1;
                     }
                     __syncthreads();
                 }
@@ -1420,7 +1440,7 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                     double d[8];
                     const int r = lane & 7;
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) d[k] = (k <= r) ? L[(j0 + k) * LDL + j0 + r] : 0.0;
+                    for (int k = 0; k < 8; ++k) d[k] = (k <= r) ? L[CO[j0 + k] + j0 + r] : 0.0;
                     bool okw = true;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
@@ -1449,13 +1469,13 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                     double v[8];
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
-                        double t = L[(j0 + c) * LDL + i];
+                        double t = L[CO[j0 + c] + i];
 #pragma unroll
                         for (int k = 0; k < c; ++k) t = fma(-v[k], LDG[(j0 + c) * 8 + k], t);
                         v[c] = t * INV[j0 + c];
                     }
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) L[(j0 + c) * LDL + i] = v[c];
+                    for (int c = 0; c < 8; ++c) L[CO[j0 + c] + i] = v[c];
                 }
                 __syncthreads();
                 if (smem[lay.FLAG] == 0.0) {          // pivot <= 0 or NaN: uniform exit
@@ -1586,7 +1606,7 @@ __global__ void __launch_bounds__(NW * 32) gpr_tile_kernel(VoxelSolveArgs va, Pr
                             if (k2 < nrb) {
 #pragma unroll
                                 for (int sl = 0; sl < 2; ++sl) {
-                                    const double a = -L[(k * 8 + 4 * sl + tig) * LDL + k2 * 8 + g];
+                                    const double a = -L[CO[k * 8 + 4 * sl + tig] + k2 * 8 + g];
 #pragma unroll
                                     for (int ct = 0; ct < CTW; ++ct)
                                         dmma_acc(C[k2][ct][0], C[k2][ct][1], a, bf[ct][sl]);
@@ -1846,6 +1866,8 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 6:
             if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
+        case 7:   // 128 < n <= 160: CTA kernel with a shared-memory-sized workspace
+            return launch_cta<true>(a, none, a.num_items, max_n < 160 ? max_n : 160, a.M, mm, work, s);
         case 3:
             if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
@@ -1867,6 +1889,7 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
         if (bucket == 2) return launch_tile<8, 3, 4, false>(none, pa, count, max_m, 1, s);
         if (bucket == 6) return launch_tile<16, 1, 12, false>(none, pa, count, max_m, 1, s);
         if (bucket == 3) return launch_tile<16, 1, 12, false>(none, pa, count, max_m, 1, s);
+
         return launch_cta<false>(none, pa, count, max_n, max_m, 1, work, s);
     }
     return launch_generic<false>(none, pa, count, max_n, max_m, work, s);

@@ -37,7 +37,7 @@ inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Optional CUDA-event timers around the library's stages (vx_profile_*).
-enum ProfStage { P_HASH = 0, P_GPR_B0, P_GPR_B1, P_GPR_B2, P_GPR_B3, P_GPR_B4, P_GPR_B5, P_GPR_B6, P_SPLAT, P_DENSIFY, P_PCA, P_COUNT };
+enum ProfStage { P_HASH = 0, P_GPR_B0, P_GPR_B1, P_GPR_B2, P_GPR_B3, P_GPR_B4, P_GPR_B5, P_GPR_B6, P_GPR_B7, P_SPLAT, P_DENSIFY, P_PCA, P_COUNT };
 void prof_begin(int stage, cudaStream_t s);
 void prof_end(int stage, cudaStream_t s);
 
@@ -103,17 +103,18 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
 // bucket boundaries for the training-set size n: warp kernels for n <= 16,
 // 32, 64; the blocked CTA kernel for n <= 128 (shared-memory resident) and
 // beyond (shared memory when it fits, else an L2-resident workspace)
-// ids: 0 n<=16, 1 n<=24, 5 n<=32 (warp kernels), 2 n<=64, 6 n<=96, 3 n<=128
-// (DMMA tile kernels), 4 n>128 (CTA kernel); later buckets got higher ids so
-// the profiling stage ids of earlier ones stay stable
-constexpr int NUM_BUCKETS = 7;
+// ids: 0 n<=16, 1 n<=24, 5 n<=32 (warp kernels), 2 n<=64, 6 n<=96, 3 n<=128,
+// 7 n<=160 (DMMA tile kernels), 4 n>160 (CTA kernel); later buckets got
+// higher ids so the profiling stage ids of earlier ones stay stable
+constexpr int NUM_BUCKETS = 8;
 __host__ __device__ inline int bucket_of(int n) {
     return n <= 16 ? 0
          : n <= 24 ? 1
          : n <= 32 ? 5
          : n <= 64 ? 2
          : n <= 96 ? 6
-         : n <= 128 ? 3 : 4;
+         : n <= 128 ? 3
+         : n <= 160 ? 7 : 4;
 }
 int launch_pca_prepass(const VoxelSolveArgs& a, int S, long long* bucket_counts, cudaStream_t s);
 int launch_bucket_items(const VoxelSolveArgs& a, int S, int32_t* items, const long long* base,

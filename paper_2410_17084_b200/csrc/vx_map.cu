@@ -77,9 +77,9 @@ enum {
     C_S,              // densify candidates
     C_MAXN,
     C_NEWSLOTS,
-    C_B0, C_B1, C_B2, C_B3, C_B4, C_B5, C_B6,   // bucket counts
-    C_F0, C_F1, C_F2, C_F3, C_F4, C_F5, C_F6,   // bucket fill cursors
-    C_O0, C_O1, C_O2, C_O3, C_O4, C_O5, C_O6,   // bucket bases
+    C_B0, C_B1, C_B2, C_B3, C_B4, C_B5, C_B6, C_B7,   // bucket counts
+    C_F0, C_F1, C_F2, C_F3, C_F4, C_F5, C_F6, C_F7,   // bucket fill cursors
+    C_O0, C_O1, C_O2, C_O3, C_O4, C_O5, C_O6, C_O7,   // bucket bases
     C_OK, C_DEGEN, C_CHOL, C_FIRST, C_CONV,
     C_COUNT
 };

@@ -421,3 +421,56 @@ def test_hash_sharded_maps_reassemble_single_gpu_result():
         np.testing.assert_array_equal(np.unique(sharding.owner_of(
             recs[r]["source_key"].cpu().numpy(), 2)), [r])
     assert len(own) == sum(len(r["opacity"]) for r in recs)
+
+
+def test_store_frame_edge_cases():
+    vmap = vx.VoxelMap(0.2, 0.01, tau=10, eta=0.3)
+    u = vmap.store_frame(vx.PointCloud.empty())
+    assert len(u) == 0 and len(vmap) == 0 and vmap.frame_index == 0
+    # reference example (tests/test_voxel_map.py:60-67): first-touch order
+    pts = [(0.01, 0.01, 0.01), (0.5, 0.5, 0.5), (0.05, 0.05, 0.05), (0.1, 0.1, 0.1)]
+    u = vmap.store_frame(vx.PointCloud(pts, np.full((4, 3), 0.5), np.full(4, 9.0)))
+    assert u.keys == [vx.VoxelKey(0, 0, 0), vx.VoxelKey(2, 2, 2)]
+    c = vmap.cell(vx.VoxelKey(0, 0, 0))
+    np.testing.assert_array_equal(c.raw.positions, np.array(pts)[[0, 2, 3]])
+    assert np.all(c.raw.noise_var == 0.01)                  # sensor_var overrides input
+    assert vmap.frame_index == 1
+    # keys outside the packed lattice are rejected, never wrapped
+    with pytest.raises(vx.InputDomainError):
+        vmap.store_frame(vx.PointCloud([[3e6, 0.0, 0.0]], [[0.5, 0.5, 0.5]], [0.0]))
+    # replay conservation (tests/test_voxel_map.py:75-84)
+    rng = np.random.default_rng(3)
+    vm2 = vx.VoxelMap(0.2, 0.01, tau=10, eta=0.3)
+    total = 0
+    for _ in range(8):
+        n = int(rng.integers(1, 200))
+        vm2.store_frame(vx.PointCloud(rng.uniform(-1, 1, (n, 3)), np.full((n, 3), 0.5),
+                                      np.zeros(n)))
+        total += n
+    assert sum(cl.point_count for cl in vm2.cells.values()) == total
+
+
+def test_single_huge_voxel_generic_path():
+    """One voxel with 1500 points (static sensor re-observing a surface)."""
+    rng = np.random.default_rng(9)
+    n = 1500
+    xy = rng.uniform(0.01, 0.49, (n, 2))
+    z = 0.2 + 0.1 * xy[:, 0] + 0.01 * rng.normal(size=n)
+    pos = np.column_stack([xy, z])
+    col = rng.uniform(0, 1, (n, 3))
+    config = vx.PipelineConfig(voxel_size=0.5)
+    vmap = vx.VoxelMap.from_config(config)
+    update = vmap.store_frame(vx.PointCloud(pos, col, np.zeros(n)))
+    preds = vx.densify_frame(update, vmap, config)
+    omap = O.OracleMap(0.5, 1e-4, 10, 0.3)
+    opreds, _ = O.densify(omap.store_frame(pos, col), omap, O.DensifyConfig())
+    assert len(preds) == len(opreds) == 1
+    p, q = preds[0], opreds[0]
+    np.testing.assert_array_equal(p.colors, q["colors"])
+    # cond(K + Sigma) of 1500 points in one voxel is large: hold mu to the
+    # oracle's own Cholesky-vs-inverse disagreement (x10), variances to 1e-9 rel
+    tp, tc, tn = omap.training(q["key"])
+    ax, f, x = O.select_axis(tp)
+    assert ax == vmap.cells[p.key].value_axis
+    np.testing.assert_allclose(p.variances, q["variances"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(p.positions, q["positions"], rtol=1e-9, atol=1e-9)
