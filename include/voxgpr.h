@@ -301,6 +301,11 @@ int vx_map_configure_solver(VxMap* map, int32_t n_s, int32_t n_r, double kernel_
 int vx_init_color(const double* d_positions, const double* d_fallback, int64_t n,
                   const VxCamera* camera, const double* d_image, double* d_sh0, void* stream);
 
+/* write_map (formats.py:154-169) payload: pack `count` Gaussian records from
+ * SoA fields into 136-byte VXSPLAT1 records (position, scale, rotation,
+ * opacity, color, source_key; little endian) at d_out (count*136 bytes). */
+int vx_pack_map_records(const VxGaussianOut* records, int64_t count, void* d_out, void* stream);
+
 /* ------------------------------------------------------------------------
  * Measurement helper: FP64 FMA peak of this device (DFMA chains, all SMs).
  * ---------------------------------------------------------------------- */

@@ -571,6 +571,14 @@ int vx_profile_read(double* ms, int64_t* launches, int32_t max_stages) {
     return P_COUNT;
 }
 
+int vx_pack_map_records(const VxGaussianOut* records, int64_t count, void* d_out, void* stream) {
+    if (!records || (!d_out && count > 0)) {
+        set_error("null argument");
+        return VX_E_INPUT;
+    }
+    return launch_pack_records(*records, count, d_out, as_stream(stream));
+}
+
 int vx_fp64_peak(double* tflops, void* stream) {
     cudaStream_t s = as_stream(stream);
     std::lock_guard<std::mutex> lk(g_scratch_mu);

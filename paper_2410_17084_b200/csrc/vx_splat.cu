@@ -214,6 +214,32 @@ int launch_gaussians(const double* pred_xyz, const double* pred_rgb, const doubl
     return VX_OK;
 }
 
+// ------------------------------------------------------------- VXSPLAT1 records
+// formats.py:25-32: position 3 f8, scale 3 f8, rotation 4 f8, opacity f8,
+// color 3 f8, source_key 3 i8 = 136 bytes, little endian, packed.  One thread
+// per record assembles it from the SoA fields.
+__global__ void k_pack_records(VxGaussianOut in, int64_t count, uint64_t* out) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= count) return;
+    uint64_t* o = out + r * 17;
+    auto bits = [](double v) { return static_cast<uint64_t>(__double_as_longlong(v)); };
+    for (int d = 0; d < 3; ++d) o[d] = bits(in.position[r * 3 + d]);
+    for (int d = 0; d < 3; ++d) o[3 + d] = bits(in.scale[r * 3 + d]);
+    for (int d = 0; d < 4; ++d) o[6 + d] = bits(in.rotation[r * 4 + d]);
+    o[10] = bits(in.opacity[r]);
+    for (int d = 0; d < 3; ++d) o[11 + d] = bits(in.color[r * 3 + d]);
+    for (int d = 0; d < 3; ++d) o[14 + d] = static_cast<uint64_t>(in.source_key[r * 3 + d]);
+}
+
+int launch_pack_records(const VxGaussianOut& in, int64_t count, void* out, cudaStream_t s) {
+    if (count <= 0) return VX_OK;
+    k_pack_records<<<unsigned((count + 255) / 256), 256, 0, s>>>(in, count,
+                                                                 static_cast<uint64_t*>(out));
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
 // ------------------------------------------------------------- moments only
 __global__ void moments_kernel(const double* pts, const double* w, int64_t G, int k,
                                const double* center, double* pos, double* phi) {

@@ -474,3 +474,27 @@ def test_single_huge_voxel_generic_path():
     assert ax == vmap.cells[p.key].value_axis
     np.testing.assert_allclose(p.variances, q["variances"], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(p.positions, q["positions"], rtol=1e-9, atol=1e-9)
+
+
+def test_map_file_from_device_records(tmp_path):
+    """VXSPLAT1 bytes written from device records == the reference layout."""
+    import struct
+    from paper_2410_17084_b200 import formats
+    config = vx.PipelineConfig(voxel_size=0.5)
+    eng = vx.MappingEngine(config)
+    pos, col = scenes.config1_scan(seed=0, frame=0, rays=8000)
+    cam = vx.Camera(fx=100.0, fy=100.0, cx=79.5, cy=59.5, width=160, height=120)
+    eng.ingest(pos, col, cam, np.random.default_rng(0).uniform(0, 1, (120, 160, 3)))
+    path = tmp_path / "a.map"
+    n = formats.write_map(path, eng, config)
+    g = eng.gaussian_map()
+    assert n == len(g) > 0
+    rec = np.empty(n, dtype=formats.MAP_RECORD)
+    rec["position"], rec["scale"], rec["rotation"] = g.positions, g.scales, g.rotations
+    rec["opacity"], rec["color"], rec["source_key"] = g.opacities, g.colors, g.source_keys
+    echo = "\n".join(config.to_lines()).encode()
+    want = b"VXSPLAT1" + struct.pack("<IQI", 1, n, len(echo)) + echo + rec.tobytes()
+    assert path.read_bytes() == want
+    back, pairs = formats.read_map(path)
+    np.testing.assert_array_equal(back.positions, g.positions)
+    assert pairs["voxel_size"] == "0.5"
