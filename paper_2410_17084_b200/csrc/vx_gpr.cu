@@ -1413,30 +1413,44 @@ __global__ void __launch_bounds__(NW * 32, 1) gpr_tile_kernel(VoxelSolveArgs va,
             }
             __syncthreads();
             ok = true;
+            // DMMA update of one 8x8 row tile of panel `jp` with columns [k_lo, k_hi)
+            auto tile_update = [&](int t, int jp, int k_lo, int k_hi) {
+                const int rb = t * 8;
+                double c0 = L[CO[jp + 2 * tig] + rb + g];
+                double c1 = L[CO[jp + 2 * tig + 1] + rb + g];
+                for (int k4 = k_lo; k4 < k_hi; k4 += 4) {
+                    const double a = -L[CO[k4 + tig] + rb + g];
+                    const double b = L[CO[k4 + tig] + jp + g];
+                    dmma_acc(c0, c1, a, b);
+                }
+                L[CO[jp + 2 * tig] + rb + g] = c0;
+                L[CO[jp + 2 * tig + 1] + rb + g] = c1;
+            };
+            bool la_prev = false;   // look-ahead already applied columns < j0 - 8 to this panel
             for (int kb = 0; kb < nrb; ++kb) {
                 const int j0 = kb * 8;
-                // (a) panel update A(i, J) -= L(i, <j0) L(J, <j0)^T, row tiles over warps
+                // (a) finish the panel update A(i, J) -= L(i, <j0) L(J, <j0)^T: after a
+                // look-ahead only the previous panel's 8 columns remain
                 if (j0 > 0) {
-                    for (int t = kb + warp; t < nrb; t += NW) {
-                        const int rb = t * 8;
-                        double c0 = L[CO[j0 + 2 * tig] + rb + g];
-                        double c1 = L[CO[j0 + 2 * tig + 1] + rb + g];
-                        for (int k4 = 0; k4 < j0; k4 += 4) {
-                            const double a = -L[CO[k4 + tig] + rb + g];
-                            const double b = L[CO[k4 + tig] + j0 + g];
-                            dmma_acc(c0, c1, a, b);
-                        }
-                        L[CO[j0 + 2 * tig] + rb + g] = c0;
-                        L[CO[j0 + 2 * tig + 1] + rb + g] = c1;
-                    }
+                    const int klo = la_prev ? j0 - 8 : 0;
+                    for (int t = kb + warp; t < nrb; t += NW) tile_update(t, j0, klo, j0);
                     __syncthreads();
                 }
                 // (b) the warps that solve rows below this block (and warp 0, which
                 // publishes INV / LDG / the pivot flag) factor the 8x8 diagonal block
                 // redundantly (lane r holds row r).  Identical inputs give identical
                 // outputs, so the duplicate shared-memory stores are benign and no
-                // barrier separates the factorisation from the rows below.
-                if (warp == 0 || warp * 32 < n8 - j0 - 8) {
+                // barrier separates the factorisation from the rows below.  The other
+                // warps meanwhile apply every final column (< j0) to the NEXT panel
+                // (look-ahead), hiding the serial factorisation behind the GEMM work.
+                const int below = n8 - j0 - 8;
+                const int nfw = below > 32 ? (below + 31) / 32 : 1;
+                const bool la = (kb + 1 < nrb) && (NW > nfw) && j0 > 0;
+                if (warp >= nfw) {
+                    if (la)
+                        for (int t = kb + 1 + (warp - nfw); t < nrb; t += NW - nfw)
+                            tile_update(t, j0 + 8, 0, j0);
+                } else {
                     double d[8];
                     const int r = lane & 7;
 #pragma unroll
@@ -1478,6 +1492,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gpr_tile_kernel(VoxelSolveArgs va,
                     for (int c = 0; c < 8; ++c) L[CO[j0 + c] + i] = v[c];
                 }
                 __syncthreads();
+                la_prev = la;
                 if (smem[lay.FLAG] == 0.0) {          // pivot <= 0 or NaN: uniform exit
                     ok = false;
                     break;
