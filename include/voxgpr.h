@@ -301,6 +301,12 @@ int vx_map_configure_solver(VxMap* map, int32_t n_s, int32_t n_r, double kernel_
 int vx_init_color(const double* d_positions, const double* d_fallback, int64_t n,
                   const VxCamera* camera, const double* d_image, double* d_sh0, void* stream);
 
+/* read_ply (formats.py:66-147) payload decode: n binary little-endian
+ * vertex records of 15 bytes (f32 x,y,z; u8 r,g,b) -> d_xyz (n,3) f64 and
+ * d_rgb (n,3) f64 = u8 / 255.0.  The scan crosses PCIe at 15 B/point
+ * instead of 48 B/point. */
+int vx_decode_ply(const void* d_records, int64_t n, double* d_xyz, double* d_rgb, void* stream);
+
 /* write_map (formats.py:154-169) payload: pack `count` Gaussian records from
  * SoA fields into 136-byte VXSPLAT1 records (position, scale, rotation,
  * opacity, color, source_key; little endian) at d_out (count*136 bytes). */

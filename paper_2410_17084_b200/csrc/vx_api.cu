@@ -571,6 +571,15 @@ int vx_profile_read(double* ms, int64_t* launches, int32_t max_stages) {
     return P_COUNT;
 }
 
+int vx_decode_ply(const void* d_records, int64_t n, double* d_xyz, double* d_rgb, void* stream) {
+    if (n > 0 && (!d_records || !d_xyz || !d_rgb)) {
+        set_error("null argument");
+        return VX_E_INPUT;
+    }
+    return launch_decode_ply(static_cast<const uint8_t*>(d_records), n, d_xyz, d_rgb,
+                             as_stream(stream));
+}
+
 int vx_pack_map_records(const VxGaussianOut* records, int64_t count, void* d_out, void* stream) {
     if (!records || (!d_out && count > 0)) {
         set_error("null argument");

@@ -126,6 +126,7 @@ int launch_gaussians(const double* pred_xyz, const double* pred_rgb, const doubl
                      const int64_t* direct_keys, int64_t count, int M, const VxCamera& cam,
                      const double* image, const VxSplatConfig& cfg, const VxGaussianOut& out,
                      cudaStream_t s);
+int launch_decode_ply(const uint8_t* rec, int64_t n, double* xyz, double* rgb, cudaStream_t s);
 int launch_pack_records(const VxGaussianOut& in, int64_t count, void* out, cudaStream_t s);
 int launch_moments(const double* pts, const double* w, int64_t G, int k, const double* center,
                    double* pos, double* phi, cudaStream_t s);

@@ -109,6 +109,7 @@ int launch_init_color(const double* pos, const double* fallback, int64_t n, cons
     return VX_OK;
 }
 
+template <bool EIGEN>
 __global__ void __launch_bounds__(256) gaussians_kernel(SplatArgs a) {
     const int nsub = a.n_s * a.n_s;
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(256) gaussians_kernel(SplatArgs a) {
     for (int j = 0; j < 6; ++j) phi[j] /= wsum;
     const int64_t r = v * nsub + b;
     double scale[3], quat[4] = {1.0, 0.0, 0.0, 0.0};
-    if (a.cfg.rotation_mode == VX_ROT_EIGEN) {
+    if constexpr (EIGEN) {
         // north-star extension: Phi = R diag(s^2) R^T with a right-handed R
         double ev[3], v0[3], V[9];
         eig3_sym(phi, ev, v0, V);
@@ -208,7 +209,34 @@ int launch_gaussians(const double* pred_xyz, const double* pred_rgb, const doubl
     SplatArgs a{pred_xyz, pred_rgb, pred_var, slot_of, voxel_ids, keys, direct_keys, count,
                 M, cfg.n_s, cfg.n_r, cam, image, cfg, out};
     const int64_t threads = count * cfg.n_s * cfg.n_s;
-    gaussians_kernel<<<unsigned((threads + 255) / 256), 256, 0, s>>>(a);
+    if (cfg.rotation_mode == VX_ROT_EIGEN)
+        gaussians_kernel<true><<<unsigned((threads + 255) / 256), 256, 0, s>>>(a);
+    else
+        gaussians_kernel<false><<<unsigned((threads + 255) / 256), 256, 0, s>>>(a);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
+// ------------------------------------------------------------- PLY vertex records
+// formats.py:35-36,126-129: binary little-endian (f32 x, y, z, u8 r, g, b) =
+// 15-byte records; positions widen to f64, colours are u8 / 255.0 (exact
+// IEEE division, as NumPy's true divide).  Byte loads: records are unaligned.
+__global__ void k_decode_ply(const uint8_t* rec, int64_t n, double* xyz, double* rgb) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t* r = rec + i * 15;
+    for (int d = 0; d < 3; ++d) {
+        const uint32_t b = uint32_t(r[4 * d]) | (uint32_t(r[4 * d + 1]) << 8) |
+                           (uint32_t(r[4 * d + 2]) << 16) | (uint32_t(r[4 * d + 3]) << 24);
+        xyz[i * 3 + d] = double(__uint_as_float(b));
+        rgb[i * 3 + d] = xdiv(double(r[12 + d]), 255.0);
+    }
+}
+
+int launch_decode_ply(const uint8_t* rec, int64_t n, double* xyz, double* rgb, cudaStream_t s) {
+    if (n <= 0) return VX_OK;
+    k_decode_ply<<<unsigned((n + 255) / 256), 256, 0, s>>>(rec, n, xyz, rgb);
     count_launch();
     VX_CHECK_LAUNCH();
     return VX_OK;

@@ -1,4 +1,9 @@
-"""VXSPLAT1 map files straight from device Gaussian records.
+"""PLY scan ingest and VXSPLAT1 map files on the device.
+
+`read_ply_device` parses the PLY header on the host, stages the raw 15-byte
+binary vertex records in pinned memory, copies them H2D (15 B/point instead of
+the 48 B/point of f64 positions + colours) and widens them on the device
+(`vx_decode_ply`); `read_ply` returns the reference's host `PointCloud`.
 
 Same byte format as the reference writer/reader (formats.py:23-32, 154-198):
 8-byte magic `VXSPLAT1`, `<IQI` (version 1, record count, echo length), the
@@ -17,8 +22,81 @@ from pathlib import Path
 import numpy as np
 
 from . import _native as N
-from .errors import ContractViolationError
+from .errors import ContractViolationError, InputDomainError
 from .splat_init import GaussianMap
+
+PLY_VERTEX = np.dtype([("x", "<f4"), ("y", "<f4"), ("z", "<f4"),
+                       ("red", "u1"), ("green", "u1"), ("blue", "u1")])
+_PLY_PROPS = [("float", "x"), ("float", "y"), ("float", "z"),
+              ("uchar", "red"), ("uchar", "green"), ("uchar", "blue")]
+
+
+def _ply_header(data: bytes, path):
+    if data[:3] != b"ply":
+        raise InputDomainError(f"{path}: missing ply magic")
+    off, fmt, count, props = 0, None, None, []
+    for _ in range(101):
+        end = data.find(b"\n", off)
+        if end < 0:
+            raise InputDomainError(f"{path}: header never ends")
+        line = data[off:end].decode("ascii", "replace").strip()
+        off = end + 1
+        tok = line.split()
+        if line == "end_header":
+            break
+        if not tok or tok[0] in ("comment", "ply"):
+            continue
+        if tok[0] == "format":
+            if len(tok) < 2 or tok[1] not in ("ascii", "binary_little_endian"):
+                raise InputDomainError(f"{path}: unsupported format {line!r}")
+            fmt = tok[1]
+        elif tok[0] == "element":
+            if len(tok) != 3 or tok[1] != "vertex":
+                raise InputDomainError(f"{path}: unsupported element {line!r}")
+            count = int(tok[2])
+        elif tok[0] == "property":
+            props.append(tuple(tok[1:]))
+    else:
+        raise InputDomainError(f"{path}: header too long")
+    if fmt is None or count is None or props != _PLY_PROPS:
+        raise InputDomainError(f"{path}: unsupported PLY layout {props!r}")
+    return fmt, count, off
+
+
+def read_ply_device(path):
+    """(d_xyz (n,3) f64, d_rgb (n,3) f64, n) on the device from a PLY file."""
+    import torch
+    lib = N.lib()
+    data = Path(path).read_bytes()
+    fmt, count, off = _ply_header(data, path)
+    dev = N.device()
+    xyz = torch.empty((count, 3), dtype=torch.float64, device=dev)
+    rgb = torch.empty((count, 3), dtype=torch.float64, device=dev)
+    if fmt == "binary_little_endian":
+        need = count * PLY_VERTEX.itemsize
+        if len(data) - off < need:
+            raise InputDomainError(f"{path}: payload truncated")
+        host = torch.frombuffer(bytearray(data[off:off + need]), dtype=torch.uint8).pin_memory()
+        rec = host.to(dev, non_blocking=True)
+    else:
+        rows = np.loadtxt(data[off:].decode("ascii").splitlines()[:count], ndmin=2)
+        if len(rows) < count or rows.shape[1] != 6:
+            raise InputDomainError(f"{path}: bad ascii payload")
+        r = np.empty(count, dtype=PLY_VERTEX)
+        r["x"], r["y"], r["z"] = rows[:, 0], rows[:, 1], rows[:, 2]
+        r["red"], r["green"], r["blue"] = rows[:, 3], rows[:, 4], rows[:, 5]
+        rec = torch.from_numpy(r.view(np.uint8).copy()).to(dev)
+    N.check(lib.vx_decode_ply(N.ptr(rec), count, N.ptr(xyz), N.ptr(rgb), N.stream_ptr()))
+    return xyz, rgb, count
+
+
+def read_ply(path, noise_var: float = 0.0):
+    """PointCloud of a PLY scan (formats.py:66-147): positions widened from f32,
+    colours u8 / 255, noise column = noise_var."""
+    from .voxel_map import PointCloud
+    xyz, rgb, n = read_ply_device(path)
+    return PointCloud(xyz.cpu().numpy(), rgb.cpu().numpy(), np.full(n, float(noise_var)))
+
 
 MAP_MAGIC = b"VXSPLAT1"
 MAP_VERSION = 1

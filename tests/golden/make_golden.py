@@ -230,7 +230,30 @@ def scan_fixture():
     np.savez_compressed(os.path.join(HERE, "scan_frames.npz"), **out)
 
 
+def ply_fixture():
+    """PLY files written by the reference writer (formats.py:42-63) and the
+    reference reader's output (formats.py:66-147)."""
+    from voxsplat import formats as rformats
+    rng = np.random.default_rng(30)
+    pos = rng.uniform(-50, 50, (500, 3))
+    col = rng.uniform(0, 1, (500, 3))
+    cloud = rvm.PointCloud(pos, col, np.zeros(500))
+    out = {}
+    for binary, name in ((True, "scan_bin.ply"), (False, "scan_ascii.ply")):
+        path = os.path.join(HERE, name)
+        rformats.write_ply(path, cloud, binary=binary)
+        back = rformats.read_ply(path, noise_var=0.25)
+        out[name + "_positions"] = back.positions
+        out[name + "_colors"] = back.colors
+    np.savez_compressed(os.path.join(HERE, "ply_ref.npz"), **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
+    ply_fixture()
     gpr_fixture()
     keys_fixture()
     axis_fixture()

@@ -498,3 +498,15 @@ def test_map_file_from_device_records(tmp_path):
     back, pairs = formats.read_map(path)
     np.testing.assert_array_equal(back.positions, g.positions)
     assert pairs["voxel_size"] == "0.5"
+
+
+@pytest.mark.parametrize("name", ["scan_bin.ply", "scan_ascii.ply"])
+def test_read_ply_matches_reference(name):
+    """PLY ingest (device decode of the 15-byte records) == the reference reader."""
+    import os
+    from paper_2410_17084_b200 import formats
+    ref = F.load("ply_ref.npz")
+    cloud = formats.read_ply(os.path.join(F.GOLDEN, name), noise_var=0.25)
+    np.testing.assert_array_equal(cloud.positions, ref[name + "_positions"])
+    np.testing.assert_array_equal(cloud.colors, ref[name + "_colors"])
+    assert np.all(cloud.noise_var == 0.25)
