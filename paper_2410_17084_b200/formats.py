@@ -78,15 +78,15 @@ def read_ply_device(path):
             raise InputDomainError(f"{path}: payload truncated")
         host = torch.frombuffer(bytearray(data[off:off + need]), dtype=torch.uint8).pin_memory()
         rec = host.to(dev, non_blocking=True)
+        N.check(lib.vx_decode_ply(N.ptr(rec), count, N.ptr(xyz), N.ptr(rgb), N.stream_ptr()))
     else:
+        # ascii rows hold decimal text: the reference parses them straight to
+        # float64 (formats.py:140-141), so positions are not narrowed to f32
         rows = np.loadtxt(data[off:].decode("ascii").splitlines()[:count], ndmin=2)
         if len(rows) < count or rows.shape[1] != 6:
             raise InputDomainError(f"{path}: bad ascii payload")
-        r = np.empty(count, dtype=PLY_VERTEX)
-        r["x"], r["y"], r["z"] = rows[:, 0], rows[:, 1], rows[:, 2]
-        r["red"], r["green"], r["blue"] = rows[:, 3], rows[:, 4], rows[:, 5]
-        rec = torch.from_numpy(r.view(np.uint8).copy()).to(dev)
-    N.check(lib.vx_decode_ply(N.ptr(rec), count, N.ptr(xyz), N.ptr(rgb), N.stream_ptr()))
+        xyz.copy_(torch.from_numpy(np.ascontiguousarray(rows[:, :3])))
+        rgb.copy_(torch.from_numpy(rows[:, 3:].astype(np.uint8)).to(dev).double() / 255.0)
     return xyz, rgb, count
 
 
