@@ -1260,8 +1260,9 @@ __host__ __device__ inline int tile_packed(int n8) {
 }
 
 struct TileLayout {
-    int L, CO, LINV, LDG, X, F, NZ, INV, Z, EA, EB, MU, VAR, BI, COL, FLAG, total;
-    __host__ __device__ TileLayout(int N8, int mm, int mcols, int mmax, bool voxel) {
+    int L, CO, LINV, LDG, X, F, NZ, INV, Z, EA, EB, MU, VAR, BI, COL, FLAG, W, total;
+    __host__ __device__ TileLayout(int N8, int mm, int mcols, int mmax, bool voxel,
+                                   bool with_w = false) {
         int o = 0;
         L = o; o += tile_packed(N8);
         CO = o; o += N8 / 2 + 1;        // int32 column offsets: L(i, j) = L[CO[j] + i]
@@ -1282,6 +1283,9 @@ struct TileLayout {
         VAR = o; o += mcols;
         BI = o; o += mcols;
         FLAG = o; o += 2;
+        o = (o + 1) & ~1;
+        W = o;
+        if (with_w) o += N8 * mcols;    // row-major right-hand-side block (big kernel)
         total = (o + 1) & ~1;
     }
 };
@@ -1744,6 +1748,430 @@ __global__ void __launch_bounds__(NW * 32, 1) gpr_tile_kernel(VoxelSolveArgs va,
     }
 }
 
+template <int NW, bool VOXEL>
+__global__ void __launch_bounds__(NW * 32, 1) gpr_big_kernel(VoxelSolveArgs va, ProblemArgs pa,
+                                                          int mmax, int mm, int nmax,
+                                                          double* gwork, int64_t per_cta) {
+    constexpr int CTW = 1;
+    constexpr int NT = NW * 32;
+    constexpr int PCOLS = NW * CTW * 8;             // right-hand sides per pass
+    const int N8 = ((nmax + 7) / 8) * 8;
+    const TileLayout lay(N8, mm, PCOLS, mmax, VOXEL, true);
+    double* smem = gwork + int64_t(blockIdx.x) * per_cta;   // per-CTA L2-resident workspace
+    double* Wg = smem + lay.W;
+    double* L = smem + lay.L;
+    double* X = smem + lay.X;
+    double* F = smem + lay.F;
+    double* NZ = smem + lay.NZ;
+    double* INV = smem + lay.INV;
+    double* Z = smem + lay.Z;
+    double* LDG = smem + lay.LDG;
+    int* CO = reinterpret_cast<int*>(smem + lay.CO);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, tig = lane & 3;
+    const int num_items = VOXEL ? va.num_items : pa.num_items;
+
+    for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
+        int n, m, s, vid = 0, cnt = 0, slot = 0, axis = 2;
+        int64_t off = 0, xo = 0, qo = 0;
+        double lam, jitter, mean_f = 0.0;
+        int kind;
+        double lo0 = 0, lo1 = 0, sp0 = 0, sp1 = 0;
+        if constexpr (VOXEL) {
+            s = va.items[it];
+            vid = va.cand_voxel[s];
+            n = va.cand_n[s];
+            cnt = va.raw_count[vid];
+            off = va.raw_offset[vid];
+            slot = va.pred_slot[vid];
+            m = va.M;
+            lam = va.lam;
+            jitter = va.jitter;
+            kind = va.kernel;
+            axis = va.cand_axis[s];
+            mean_f = va.cand_meanf[s];
+            const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
+            for (int r = tid; r < N8; r += NT) {
+                if (r < n) {
+                    const double* p = train_point(va, r, cnt, off, slot);
+                    X[2 * r] = p[pa_];
+                    X[2 * r + 1] = p[pb_];
+                    F[r] = xsub(p[axis], mean_f);
+                    NZ[r] = r < cnt ? va.sensor_var : va.pred_var[int64_t(slot) * m + (r - cnt)];
+                } else {
+                    X[2 * r] = X[2 * r + 1] = F[r] = NZ[r] = 0.0;
+                }
+            }
+            lo0 = xmul(double(va.keys[int64_t(vid) * 3 + pa_]), va.voxel_size);
+            lo1 = xmul(double(va.keys[int64_t(vid) * 3 + pb_]), va.voxel_size);
+            sp0 = xsub(xadd(lo0, va.voxel_size), lo0);
+            sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
+            __syncthreads();
+            if (kind == VX_KERNEL_SE) {
+                double* EA = smem + lay.EA;
+                double* EB = smem + lay.EB;
+                for (int e = tid; e < 2 * N8 * mm; e += NT) {
+                    const int which = e >= N8 * mm;
+                    const int rem = e - which * N8 * mm;
+                    const int i = rem / mm, r = rem - i * mm;
+                    double v = 0.0;
+                    if (i < n) {
+                        const double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
+                        const double gg = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
+                        const double d = xsub(X[2 * i + which], gg);
+                        v = exp(xmul(-lam, xmul(d, d)));
+                    }
+                    (which ? EB : EA)[i * mm + r] = v;
+                }
+            }
+        } else {
+            s = pa.items[it];
+            xo = pa.x_off[s];
+            qo = pa.q_off[s];
+            n = int(pa.x_off[s + 1] - xo);
+            m = int(pa.q_off[s + 1] - qo);
+            lam = pa.lam[s];
+            jitter = pa.jitter;
+            kind = pa.kernel;
+            for (int r = tid; r < N8; r += NT) {
+                if (r < n) {
+                    X[2 * r] = pa.x[(xo + r) * 2];
+                    X[2 * r + 1] = pa.x[(xo + r) * 2 + 1];
+                    F[r] = pa.f[xo + r];
+                    NZ[r] = pa.noise[xo + r];
+                } else {
+                    X[2 * r] = X[2 * r + 1] = F[r] = NZ[r] = 0.0;
+                }
+            }
+        }
+        const int nrb = (n + 7) >> 3;
+        const int n8 = nrb * 8;
+        for (int j = tid; j < n8; j += NT) {
+            const int kb = j >> 3;
+            int o = 0;
+            for (int t = 0; t < kb; ++t) o += 8 * tile_ldb(n8, t);
+            CO[j] = o + (j & 7) * tile_ldb(n8, kb) - 8 * kb;
+        }
+        __syncthreads();
+
+        // ---- A (identity-padded), panel Cholesky with DMMA updates, one retry
+        bool ok = false;
+        for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+            const double jit = attempt ? jitter : 0.0;
+            const int tot = n8 * (n8 + 1) / 2;
+            for (int e = tid; e < tot; e += NT) {
+                // lower-triangle index -> (i, j): single-precision root + one fix-up
+                int i = int((sqrtf(8.0f * float(e) + 1.0f) - 1.0f) * 0.5f);
+                if ((i + 1) * (i + 2) / 2 <= e) ++i;
+                if (i * (i + 1) / 2 > e) --i;
+                const int j = e - i * (i + 1) / 2;
+                double v;
+                if (i >= n) {
+                    v = (i == j) ? 1.0 : 0.0;
+                } else if (i == j) {
+                    v = xadd(1.0, NZ[i]);
+                    if (jit != 0.0) v = xadd(v, jit);
+                } else {
+                    v = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
+                }
+                L[CO[j] + i] = v;
+            }
+            __syncthreads();
+            ok = true;
+            // DMMA update of one 8x8 row tile of panel `jp` with columns [k_lo, k_hi)
+            auto tile_update = [&](int t, int jp, int k_lo, int k_hi) {
+                const int rb = t * 8;
+                double c0 = L[CO[jp + 2 * tig] + rb + g];
+                double c1 = L[CO[jp + 2 * tig + 1] + rb + g];
+                for (int k4 = k_lo; k4 < k_hi; k4 += 4) {
+                    const double a = -L[CO[k4 + tig] + rb + g];
+                    const double b = L[CO[k4 + tig] + jp + g];
+                    dmma_acc(c0, c1, a, b);
+                }
+                L[CO[jp + 2 * tig] + rb + g] = c0;
+                L[CO[jp + 2 * tig + 1] + rb + g] = c1;
+            };
+            bool la_prev = false;   // look-ahead already applied columns < j0 - 8 to this panel
+            for (int kb = 0; kb < nrb; ++kb) {
+                const int j0 = kb * 8;
+                // (a) finish the panel update A(i, J) -= L(i, <j0) L(J, <j0)^T: after a
+                // look-ahead only the previous panel's 8 columns remain
+                if (j0 > 0) {
+                    const int klo = la_prev ? j0 - 8 : 0;
+                    for (int t = kb + warp; t < nrb; t += NW) tile_update(t, j0, klo, j0);
+                    __syncthreads();
+                }
+                // (b) the warps that solve rows below this block (and warp 0, which
+                // publishes INV / LDG / the pivot flag) factor the 8x8 diagonal block
+                // redundantly (lane r holds row r).  Identical inputs give identical
+                // outputs, so the duplicate shared-memory stores are benign and no
+                // barrier separates the factorisation from the rows below.  The other
+                // warps meanwhile apply every final column (< j0) to the NEXT panel
+                // (look-ahead), hiding the serial factorisation behind the GEMM work.
+                const int below = n8 - j0 - 8;
+                const int nfw = below > 32 ? (below + 31) / 32 : 1;
+                const bool la = (kb + 1 < nrb) && (NW > nfw) && j0 > 0;
+                if (warp >= nfw) {
+                    if (la)
+                        for (int t = kb + 1 + (warp - nfw); t < nrb; t += NW - nfw)
+                            tile_update(t, j0 + 8, 0, j0);
+                } else {
+                    double d[8];
+                    const int r = lane & 7;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) d[k] = (k <= r) ? L[CO[j0 + k] + j0 + r] : 0.0;
+                    bool okw = true;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const double piv = __shfl_sync(FULL, d[c], c);
+                        if (!(piv > 0.0)) okw = false;
+                        const double inv = rsqrt(piv);          // dpotf2 scales by 1/ajj
+                        const double lcc = piv * inv;
+                        if (r == c) d[c] = lcc;
+                        else if (r > c) d[c] = d[c] * inv;
+#pragma unroll
+                        for (int k = c + 1; k < 8; ++k) {
+                            const double lkc = __shfl_sync(FULL, d[c], k);
+                            if (r >= k) d[k] = fma(-d[c], lkc, d[k]);
+                        }
+                        if (lane == c) INV[j0 + c] = inv;
+                    }
+                    if (lane < 8) {                   // separate buffer: other warps may
+#pragma unroll                                        // still be reading the block in L
+                        for (int k = 0; k < 8; ++k) LDG[(j0 + r) * 8 + k] = (k <= r) ? d[k] : 0.0;
+                    }
+                    if (warp == 0 && lane == 0) smem[lay.FLAG] = okw ? 1.0 : 0.0;
+                    __syncwarp();
+                }
+                // (c) rows below the block: L(i, J) = A(i, J) L_JJ^-T
+                for (int i = j0 + 8 + tid; i < n8; i += NT) {
+                    double v[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        double t = L[CO[j0 + c] + i];
+#pragma unroll
+                        for (int k = 0; k < c; ++k) t = fma(-v[k], LDG[(j0 + c) * 8 + k], t);
+                        v[c] = t * INV[j0 + c];
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) L[CO[j0 + c] + i] = v[c];
+                }
+                __syncthreads();
+                la_prev = la;
+                if (smem[lay.FLAG] == 0.0) {          // pivot <= 0 or NaN: uniform exit
+                    ok = false;
+                    break;
+                }
+            }
+            __syncthreads();
+        }
+        if (!ok) {
+            if (tid == 0) {
+                if constexpr (VOXEL) {
+                    va.cand_status[s] = VX_ST_CHOL_FAIL;
+                    const uint8_t st = va.state[vid];
+                    va.cand_before[s] = st;
+                    va.cand_after[s] = st;
+                } else {
+                    pa.status[s] = VX_ST_CHOL_FAIL;
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+        // inverses of the diagonal blocks (thread = (block, column)): L_kk x = e_c
+        double* LINV = smem + lay.LINV;
+        for (int t = tid; t < nrb * 8; t += NT) {
+            const int kb = t >> 3, c = t & 7, b0 = kb * 8;
+            double x[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                double v = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+                for (int k = 0; k < r; ++k) v = fma(-LDG[(b0 + r) * 8 + k], x[k], v);
+                x[r] = (r < c) ? 0.0 : v * INV[b0 + r];
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) LINV[(b0 + r) * 8 + c] = x[r];
+        }
+        __syncthreads();
+
+        // ---- forward substitution, left-looking: C_k = B_k - sum_j L_kj W_j by DMMA
+        // (two accumulator chains), W_k = L_kk^-1 C_k, W kept row-major in the workspace
+        const int ncols = m + 1;
+        const double* EA = smem + lay.EA;
+        const double* EB = smem + lay.EB;
+        for (int c0 = 0; c0 < ncols; c0 += PCOLS) {
+            const int ctile = warp;                       // one 8-column tile per warp
+            int ri[2] = {0, 0}, si[2] = {0, 0};
+            double g0[2] = {0, 0}, g1[2] = {0, 0};
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = c0 + ctile * 8 + 2 * tig + e;
+                const int q = c - 1;
+                if (c > 0 && c < ncols) {
+                    if constexpr (VOXEL) {
+                        const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+                        const int sr = q / (ns * nr2);
+                        const int rem = q - sr * ns * nr2;
+                        const int sc = rem / nr2;
+                        const int rem2 = rem - sc * nr2;
+                        const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                        ri[e] = sr * nr + fr;
+                        si[e] = sc * nr + fc;
+                        g0[e] = xadd(lo0, xdiv(xmul(double(ri[e]) + 0.5, sp0), double(mm)));
+                        g1[e] = xadd(lo1, xdiv(xmul(double(si[e]) + 0.5, sp1), double(mm)));
+                    } else {
+                        g0[e] = pa.xs[(qo + q) * 2];
+                        g1[e] = pa.xs[(qo + q) * 2 + 1];
+                    }
+                }
+            }
+            double ssp[2] = {0.0, 0.0};
+            for (int k = 0; k < nrb; ++k) {
+                double ca[2], cb[2] = {0.0, 0.0};
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = c0 + ctile * 8 + 2 * tig + e;
+                    const int i = k * 8 + g;
+                    double v = 0.0;
+                    if (i < n && c < ncols) {
+                        if (c == 0) v = F[i];
+                        else if (VOXEL && kind == VX_KERNEL_SE) v = EA[i * mm + ri[e]] * EB[i * mm + si[e]];
+                        else v = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], g0[e], g1[e]));
+                    }
+                    ca[e] = v;
+                }
+                for (int j = 0; j < k; ++j) {
+#pragma unroll
+                    for (int sl = 0; sl < 2; ++sl) {
+                        const int kk = j * 8 + 4 * sl + tig;
+                        const double a = -L[CO[kk] + k * 8 + g];
+                        const double bw = Wg[int64_t(kk) * PCOLS + ctile * 8 + g];
+                        if (sl == 0) dmma_acc(ca[0], ca[1], a, bw);
+                        else dmma_acc(cb[0], cb[1], a, bw);
+                    }
+                }
+                ca[0] += cb[0];
+                ca[1] += cb[1];
+                // W_k = L_kk^-1 C_k (C_k -> B fragments by shuffles)
+                double bc[2];
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl) {
+                    const int src = (4 * sl + tig) * 4 + (g >> 1);
+                    const double v0 = __shfl_sync(FULL, ca[0], src);
+                    const double v1 = __shfl_sync(FULL, ca[1], src);
+                    bc[sl] = (g & 1) ? v1 : v0;
+                }
+                double d0 = 0.0, d1 = 0.0;
+                dmma_acc(d0, d1, LINV[(k * 8 + g) * 8 + tig], bc[0]);
+                dmma_acc(d0, d1, LINV[(k * 8 + g) * 8 + 4 + tig], bc[1]);
+                Wg[int64_t(k * 8 + g) * PCOLS + ctile * 8 + 2 * tig] = d0;
+                Wg[int64_t(k * 8 + g) * PCOLS + ctile * 8 + 2 * tig + 1] = d1;
+                ssp[0] = fma(d0, d0, ssp[0]);
+                ssp[1] = fma(d1, d1, ssp[1]);
+                __syncwarp();
+            }
+            __syncthreads();
+            if (c0 == 0)
+                for (int i = tid; i < n8; i += NT) Z[i] = Wg[int64_t(i) * PCOLS];   // z = L^-1 f
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double ss = ssp[e], mu = 0.0;
+                for (int k = 0; k < nrb; ++k)
+                    mu = fma(Wg[int64_t(k * 8 + g) * PCOLS + ctile * 8 + 2 * tig + e], Z[k * 8 + g], mu);
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) {
+                    ss += __shfl_xor_sync(FULL, ss, o);
+                    mu += __shfl_xor_sync(FULL, mu, o);
+                }
+                const int lc = ctile * 8 + 2 * tig + e;
+                const int c = c0 + lc;
+                if (g == 0 && c > 0 && c < ncols) {
+                    const double var = 1.0 - ss;
+                    if constexpr (VOXEL) {
+                        smem[lay.MU + lc] = xadd(mu, mean_f);
+                        smem[lay.VAR + lc] = var < 0.0 ? 0.0 : var;
+                    } else {
+                        pa.mu[qo + c - 1] = mu;
+                        pa.var[qo + c - 1] = var;
+                    }
+                }
+            }
+            if constexpr (VOXEL) {
+                // voxel mode: m + 1 <= PCOLS (asserted by the launcher), one pass
+                __syncthreads();
+                double* COL = smem + lay.COL;
+                int* BI = reinterpret_cast<int*>(smem + lay.BI);
+                for (int q = tid; q < m; q += NT) {
+                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+                    const int sr = q / (ns * nr2);
+                    const int rem = q - sr * ns * nr2;
+                    const int sc = rem / nr2;
+                    const int rem2 = rem - sc * nr2;
+                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                    const double g0 = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
+                    const double g1 = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
+                    double best = INFINITY;
+                    int bi = 0;
+                    for (int t = 0; t < n; ++t) {
+                        const double d2 = dist2_exact(g0, g1, X[2 * t], X[2 * t + 1]);
+                        if (d2 < best) { best = d2; bi = t; }
+                    }
+                    BI[q] = bi;
+                    const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
+                                                : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
+                    COL[q * 3] = cs[0];
+                    COL[q * 3 + 1] = cs[1];
+                    COL[q * 3 + 2] = cs[2];
+                }
+                __syncthreads();
+                const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
+                double* oxyz = va.pred_xyz + int64_t(slot) * m * 3;
+                double* orgb = va.pred_rgb + int64_t(slot) * m * 3;
+                double* ovar = va.pred_var + int64_t(slot) * m;
+                for (int q = tid; q < m; q += NT) {
+                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+                    const int sr = q / (ns * nr2);
+                    const int rem = q - sr * ns * nr2;
+                    const int sc = rem / nr2;
+                    const int rem2 = rem - sc * nr2;
+                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
+                    double pos[3];
+                    pos[axis] = smem[lay.MU + q + 1];
+                    pos[pa_] = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
+                    pos[pb_] = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
+                    oxyz[q * 3] = pos[0];
+                    oxyz[q * 3 + 1] = pos[1];
+                    oxyz[q * 3 + 2] = pos[2];
+                    orgb[q * 3] = COL[q * 3];
+                    orgb[q * 3 + 1] = COL[q * 3 + 1];
+                    orgb[q * 3 + 2] = COL[q * 3 + 2];
+                    ovar[q] = smem[lay.VAR + q + 1];
+                }
+                if (tid == 0) {
+                    const double* V = smem + lay.VAR + 1;
+                    const double mv = xdiv(np_pairwise_sum([V](int i) { return V[i]; }, m), double(m));
+                    const uint8_t before = va.state[vid];
+                    const uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
+                    va.state[vid] = after;
+                    va.value_axis[vid] = int8_t(axis);
+                    va.has_pred[vid] = 1;
+                    va.cand_status[s] = VX_ST_OK;
+                    va.cand_before[s] = before;
+                    va.cand_after[s] = after;
+                }
+            }
+            __syncthreads();
+        }
+        if constexpr (!VOXEL) {
+            if (tid == 0) pa.status[s] = VX_ST_OK;
+        }
+        __syncthreads();
+    }
+}
+
 template <int NRB, int CTW, int NW, bool VOXEL>
 static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int m_max,
                        int mm, cudaStream_t s) {
@@ -1764,6 +2192,31 @@ static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     const int cap = sm_count() * per_sm;
     if (blocks > cap) blocks = cap;
     kfn<<<blocks, NW * 32, smem, s>>>(va, pa, m_max, mm);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
+template <int NW, bool VOXEL>
+static int launch_big(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int n_max,
+                      int m_max, int mm, DevBuf& work, cudaStream_t s) {
+    if (num_items <= 0) return VX_OK;
+    constexpr int PCOLS = NW * 8;
+    if (VOXEL && m_max + 1 > PCOLS) {
+        set_error("big kernel: %d right-hand sides exceed %d", m_max + 1, PCOLS);
+        return VX_E_INPUT;
+    }
+    const int n8 = ((n_max + 7) / 8) * 8;
+    const TileLayout lay(n8, mm, PCOLS, m_max, VOXEL, true);
+    const int64_t per = lay.total;
+    int blocks = num_items;
+    int cap = sm_count() * 2;
+    const int64_t max_blocks = (int64_t(4) << 30) / (per * 8);
+    if (cap > max_blocks) cap = int(max_blocks > 0 ? max_blocks : 1);
+    if (blocks > cap) blocks = cap;
+    VX_TRY(work.reserve(size_t(per) * 8 * blocks, s));
+    gpr_big_kernel<NW, VOXEL><<<blocks, NW * 32, 0, s>>>(va, pa, m_max, mm, n_max, work.as<double>(),
+                                                         per);
     count_launch();
     VX_CHECK_LAUNCH();
     return VX_OK;
@@ -1881,12 +2334,16 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 6:
             if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
-        case 7:   // 128 < n <= 160: CTA kernel with a shared-memory-sized workspace
+        case 7:   // 128 < n <= 160
+            if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n < 160 ? max_n : 160,
+                                                           a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 160 ? max_n : 160, a.M, mm, work, s);
         case 3:
             if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
-        default: return launch_cta<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
+        default:
+            if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n, a.M, mm, work, s);
+            return launch_cta<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
     }
 }
 
@@ -1905,7 +2362,7 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
         if (bucket == 6) return launch_tile<16, 1, 12, false>(none, pa, count, max_m, 1, s);
         if (bucket == 3) return launch_tile<16, 1, 12, false>(none, pa, count, max_m, 1, s);
 
-        return launch_cta<false>(none, pa, count, max_n, max_m, 1, work, s);
+        return launch_big<12, false>(none, pa, count, max_n, max_m, 1, work, s);
     }
     return launch_generic<false>(none, pa, count, max_n, max_m, work, s);
 }
