@@ -85,8 +85,11 @@ def read_ply_device(path):
         rows = np.loadtxt(data[off:].decode("ascii").splitlines()[:count], ndmin=2)
         if len(rows) < count or rows.shape[1] != 6:
             raise InputDomainError(f"{path}: bad ascii payload")
-        xyz.copy_(torch.from_numpy(np.ascontiguousarray(rows[:, :3])))
-        rgb.copy_(torch.from_numpy(rows[:, 3:].astype(np.uint8)).to(dev).double() / 255.0)
+        r = np.zeros(count, dtype=PLY_VERTEX)
+        r["red"], r["green"], r["blue"] = rows[:, 3], rows[:, 4], rows[:, 5]
+        rec = torch.from_numpy(r.view(np.uint8).copy()).to(dev)
+        N.check(lib.vx_decode_ply(N.ptr(rec), count, N.ptr(xyz), N.ptr(rgb), N.stream_ptr()))
+        xyz.copy_(torch.from_numpy(np.ascontiguousarray(rows[:, :3])))   # u8/255 colours kept
     return xyz, rgb, count
 
 
