@@ -1748,17 +1748,21 @@ __global__ void __launch_bounds__(NW * 32, 1) gpr_tile_kernel(VoxelSolveArgs va,
     }
 }
 
-template <int NW, bool VOXEL>
-__global__ void __launch_bounds__(NW * 32, 1) gpr_big_kernel(VoxelSolveArgs va, ProblemArgs pa,
-                                                          int mmax, int mm, int nmax,
-                                                          double* gwork, int64_t per_cta) {
+template <int NW, bool VOXEL, bool SMEM>
+__global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
+        VoxelSolveArgs va, ProblemArgs pa, int mmax, int mm, int nmax, double* gwork,
+        int64_t per_cta) {
+    // SMEM: everything but W in dynamic shared memory, W in a per-CTA global
+    // slice; otherwise every buffer lives in the per-CTA global workspace.
+    extern __shared__ __align__(16) double dsm[];
     constexpr int CTW = 1;
     constexpr int NT = NW * 32;
     constexpr int PCOLS = NW * CTW * 8;             // right-hand sides per pass
     const int N8 = ((nmax + 7) / 8) * 8;
-    const TileLayout lay(N8, mm, PCOLS, mmax, VOXEL, true);
-    double* smem = gwork + int64_t(blockIdx.x) * per_cta;   // per-CTA L2-resident workspace
-    double* Wg = smem + lay.W;
+    const int MC = (mmax + 1 > PCOLS ? mmax + 1 : PCOLS);
+    const TileLayout lay(N8, mm, MC, mmax, VOXEL, !SMEM);
+    double* smem = SMEM ? dsm : gwork + int64_t(blockIdx.x) * per_cta;
+    double* Wg = SMEM ? gwork + int64_t(blockIdx.x) * per_cta : smem + lay.W;
     double* L = smem + lay.L;
     double* X = smem + lay.X;
     double* F = smem + lay.F;
@@ -2091,16 +2095,19 @@ __global__ void __launch_bounds__(NW * 32, 1) gpr_big_kernel(VoxelSolveArgs va, 
                 if (g == 0 && c > 0 && c < ncols) {
                     const double var = 1.0 - ss;
                     if constexpr (VOXEL) {
-                        smem[lay.MU + lc] = xadd(mu, mean_f);
-                        smem[lay.VAR + lc] = var < 0.0 ? 0.0 : var;
+                        smem[lay.MU + c] = xadd(mu, mean_f);
+                        smem[lay.VAR + c] = var < 0.0 ? 0.0 : var;
                     } else {
                         pa.mu[qo + c - 1] = mu;
                         pa.var[qo + c - 1] = var;
                     }
                 }
             }
+            __syncthreads();
+        }
+        {
             if constexpr (VOXEL) {
-                // voxel mode: m + 1 <= PCOLS (asserted by the launcher), one pass
+                // every pass has written MU / VAR (indexed by column): epilogue once
                 __syncthreads();
                 double* COL = smem + lay.COL;
                 int* BI = reinterpret_cast<int*>(smem + lay.BI);
@@ -2202,21 +2209,28 @@ static int launch_big(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_i
                       int m_max, int mm, DevBuf& work, cudaStream_t s) {
     if (num_items <= 0) return VX_OK;
     constexpr int PCOLS = NW * 8;
-    if (VOXEL && m_max + 1 > PCOLS) {
-        set_error("big kernel: %d right-hand sides exceed %d", m_max + 1, PCOLS);
-        return VX_E_INPUT;
-    }
     const int n8 = ((n_max + 7) / 8) * 8;
-    const TileLayout lay(n8, mm, PCOLS, m_max, VOXEL, true);
-    const int64_t per = lay.total;
+    const int MC = m_max + 1 > PCOLS ? m_max + 1 : PCOLS;
+    // shared-memory variant when everything but W fits two CTAs per SM
+    const TileLayout small(n8, mm, MC, m_max, VOXEL, false);
+    const size_t smem = size_t(small.total) * sizeof(double);
+    const bool use_smem = smem <= size_t(NW <= 6 ? 112 : 220) * 1024;
+    const TileLayout full(n8, mm, MC, m_max, VOXEL, true);
+    const int64_t per = use_smem ? int64_t(n8) * PCOLS : full.total;
     int blocks = num_items;
     int cap = sm_count() * 2;
     const int64_t max_blocks = (int64_t(4) << 30) / (per * 8);
     if (cap > max_blocks) cap = int(max_blocks > 0 ? max_blocks : 1);
     if (blocks > cap) blocks = cap;
     VX_TRY(work.reserve(size_t(per) * 8 * blocks, s));
-    gpr_big_kernel<NW, VOXEL><<<blocks, NW * 32, 0, s>>>(va, pa, m_max, mm, n_max, work.as<double>(),
-                                                         per);
+    if (use_smem) {
+        auto kfn = gpr_big_kernel<NW, VOXEL, true>;
+        VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kfn<<<blocks, NW * 32, smem, s>>>(va, pa, m_max, mm, n_max, work.as<double>(), per);
+    } else {
+        gpr_big_kernel<NW, VOXEL, false><<<blocks, NW * 32, 0, s>>>(va, pa, m_max, mm, n_max,
+                                                                    work.as<double>(), per);
+    }
     count_launch();
     VX_CHECK_LAUNCH();
     return VX_OK;
@@ -2328,18 +2342,19 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 0: return launch_warp<16, true>(a, none, a.num_items, a.M, mm, s);
         case 1: return launch_warp<24, true>(a, none, a.num_items, a.M, mm, s);
         case 5: return launch_warp<32, true>(a, none, a.num_items, a.M, mm, s);
-        case 2:
-            if (a.M + 1 <= 96) return launch_tile<8, 3, 4, true>(a, none, a.num_items, a.M, mm, s);
+        case 2:   // 32 < n <= 64: two 6-warp CTAs per SM, W streamed through L2
+            return launch_big<6, true>(a, none, a.num_items, max_n < 64 ? max_n : 64, a.M, mm, work, s);
             return launch_warp<64, true>(a, none, a.num_items, a.M, mm, s);
-        case 6:
-            if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
+        case 6:   // 64 < n <= 96: same, measured faster than the register-resident tile kernel
+            return launch_big<6, true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
         case 7:   // 128 < n <= 160
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n < 160 ? max_n : 160,
                                                            a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 160 ? max_n : 160, a.M, mm, work, s);
-        case 3:
+        case 3:   // 96 < n <= 128: register-resident DMMA tile kernel
             if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
+            return launch_big<12, true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
         default:
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n, a.M, mm, work, s);
