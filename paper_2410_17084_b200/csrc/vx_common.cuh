@@ -95,6 +95,31 @@ __device__ double np_pairwise_block(Get get, int lo, int n) {
     return res;
 }
 
+// Warp-cooperative np_pairwise_sum of a shared-memory array: the eight strided
+// accumulators live in lanes 0-7 and are combined with shuffles in NumPy's
+// order, so the result is bit-identical to np_pairwise_block.  All lanes of
+// the warp must call it; every lane gets the result.
+__device__ __forceinline__ double warp_pairwise_block(const double* a, int n) {
+    if (n < 8) {
+        double s = -0.0;
+        for (int i = 0; i < n; ++i) s = xadd(s, a[i]);
+        return s;
+    }
+    const int lane = threadIdx.x & 31;
+    const int full = n - (n % 8);
+    double r = 0.0;
+    if (lane < 8) {
+        r = a[lane];
+        for (int i = 8 + lane; i < full; i += 8) r = xadd(r, a[i]);
+    }
+    r = xadd(r, __shfl_down_sync(FULL, r, 1));   // r0+r1, r2+r3, ...
+    r = xadd(r, __shfl_down_sync(FULL, r, 2));   // (r0+r1)+(r2+r3), ...
+    r = xadd(r, __shfl_down_sync(FULL, r, 4));
+    double res = __shfl_sync(FULL, r, 0);
+    for (int i = full; i < n; ++i) res = xadd(res, a[i]);
+    return res;
+}
+
 template <typename Get>
 __device__ double np_pairwise_sum(Get get, int n) {
     // iterative form of the recursive split for n > 128 (depth <= 24)
@@ -138,6 +163,19 @@ __device__ double np_pairwise_sum(Get get, int n) {
         state[sp] = 0;
     }
     return ret;
+}
+
+// np_pairwise_sum of a shared-memory array by a whole warp (n <= 256: at most
+// one split level, as for n* <= 256); larger n falls back to the scalar form.
+__device__ __forceinline__ double warp_pairwise_sum(const double* a, int n) {
+    if (n <= 128) return warp_pairwise_block(a, n);
+    if (n <= 256) {
+        int n2 = n / 2;
+        n2 -= n2 % 8;
+        const double left = warp_pairwise_block(a, n2);
+        return xadd(left, warp_pairwise_block(a + n2, n - n2));
+    }
+    return np_pairwise_sum([a](int i) { return a[i]; }, n);
 }
 
 // ---------------------------------------------------------------------------

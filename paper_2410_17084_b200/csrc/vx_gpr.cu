@@ -1245,6 +1245,351 @@ __device__ __forceinline__ void dmma_acc(double& c0, double& c1, double a, doubl
         : "d"(a), "d"(b));
 }
 
+// ---------------------------------------------------------------------------
+// warp-per-voxel DMMA kernel (voxel mode, n <= NMAX, NMAX in {16, 24, 32})
+// ---------------------------------------------------------------------------
+// One warp per voxel, no CTA barriers inside the voxel loop.
+//   * A = K + diag(noise): the strict lower triangle is filled compactly
+//     (lane = entry, from a per-CTA (i, j) table), then lane i holds row i of
+//     A in registers and the warp factorises right-looking: column j is
+//     scaled in registers, published to shared memory (column-major L) and
+//     read back as 16-byte broadcasts for the rank-1 update of the rows.
+//   * lane c forms column c of L^-1 by substitution; L^-1 is stored row-major
+//     over L's slot and its fragments stay in registers for the whole voxel.
+//   * W^T = [f | K*]^T L^-T with m8n8k4 DMMA, 8 right-hand sides per tile:
+//     the A operand K*(i, q) = EA[ri(q)][i] * EB[si(q)][i] comes from the
+//     separable tables (stored transposed so a lane's four rows are
+//     immediate offsets), the B operand is the L^-1 fragment.  Accumulator
+//     rows are queries, so sigma^2_q = 1 - |w_q|^2 and mu_q = w_q . z
+//     (z = L^-1 f, row 0 of tile 0) reduce over the 4 lanes of a row.
+// 11 independent column tiles per voxel at n* = 81.
+template <int NMAX>
+__global__ void __launch_bounds__(128, NMAX <= 16 ? 6 : (NMAX <= 24 ? 4 : 3))
+gpr_wdmma_kernel(VoxelSolveArgs va, int mmax, int mm) {
+    extern __shared__ __align__(16) double smem[];
+    constexpr int LD = NMAX;
+    constexpr int NRB = NMAX / 8;         // 8-row blocks
+    constexpr int NKS = NMAX / 4;         // k-chunks of 4
+    constexpr int NA = NRB * (NRB + 1);   // fragments of the lower-triangular L^-1
+    constexpr int NTRI = NMAX * (NMAX - 1) / 2;
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, tig = lane & 3;
+    const int wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const WarpLayout lay(NMAX, mm, mmax, true);
+    const int ncols = va.M + 1;
+    const int ntiles = (ncols + 7) >> 3;
+    // per-CTA tables: ONE/ZERO rows, column c of [f | K*] -> (ri, si) of
+    // query c - 1, strict-lower-triangle entry e -> (i, j)
+    double* ONE = smem + size_t(wpb) * lay.total;
+    double* ZERO = ONE + NMAX;
+    int* QRI = reinterpret_cast<int*>(ZERO + NMAX);
+    int* QSI = QRI + 8 * ntiles;
+    int* TRI = QSI + 8 * ntiles;
+    for (int c = threadIdx.x; c < 8 * ntiles; c += blockDim.x) {
+        int ri = -1, si = -1;
+        if (c >= 1 && c < ncols) {
+            const int q = c - 1;
+            const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+            const int sr = q / (ns * nr2);
+            const int rem = q - sr * ns * nr2;
+            const int sc = rem / nr2;
+            const int rem2 = rem - sc * nr2;
+            const int fr = rem2 / nr, fc = rem2 - fr * nr;
+            ri = sr * nr + fr;
+            si = sc * nr + fc;
+        }
+        QRI[c] = ri;
+        QSI[c] = si;
+    }
+    for (int e = threadIdx.x; e < NTRI; e += blockDim.x) {
+        int r, j;
+        tri_decode(e, &r, &j);                 // e = r (r + 1) / 2 + j, j <= r
+        TRI[e] = (r + 1) | (j << 8);           // row i = r + 1 > j
+    }
+    for (int i = threadIdx.x; i < NMAX; i += blockDim.x) {
+        ONE[i] = 1.0;
+        ZERO[i] = 0.0;
+    }
+    __syncthreads();
+    double* base = smem + size_t(wib) * lay.total;
+    double* X = base + lay.X;
+    double* F = base + lay.F;
+    double* NZ = base + lay.NZ;
+    double* L = base + lay.L;
+    double* INV = base + lay.INV;
+    double* EA = base + lay.EA;           // EA[r * NMAX + i] = exp(-lam (x_i - c_r)^2)
+    double* EB = base + lay.EB;
+    double* GC = base + lay.GC;
+    double* MU = base + lay.MU;
+    double* VAR = base + lay.VAR;
+
+    for (int it = blockIdx.x * wpb + wib; it < va.num_items; it += gridDim.x * wpb) {
+        const int s = va.items[it];
+        const int vid = va.cand_voxel[s];
+        const int n = va.cand_n[s];
+        const int cnt = va.raw_count[vid];
+        const int64_t off = va.raw_offset[vid];
+        const int slot = va.pred_slot[vid];
+        const int m = va.M;
+        const double lam = va.lam;
+        const int kind = va.kernel;
+        const int axis = va.cand_axis[s];
+        const double mean_f = va.cand_meanf[s];
+        const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
+        // ---- stage raw ∪ pseudo (voxel_map.py:196-200), split by axis; pad with zeros
+        for (int r = lane; r < NMAX; r += 32) {
+            if (r < n) {
+                const double* p = train_point(va, r, cnt, off, slot);
+                X[2 * r] = p[pa_];
+                X[2 * r + 1] = p[pb_];
+                F[r] = xsub(p[axis], mean_f);
+                NZ[r] = r < cnt ? va.sensor_var : va.pred_var[int64_t(slot) * m + (r - cnt)];
+            } else {
+                X[2 * r] = X[2 * r + 1] = F[r] = NZ[r] = 0.0;
+            }
+        }
+        // ---- voxel grid (gpr.py:104-120, 262-266): lo + ((i + 0.5) * (hi - lo)) / m
+        const double lo0 = xmul(double(va.keys[int64_t(vid) * 3 + pa_]), va.voxel_size);
+        const double lo1 = xmul(double(va.keys[int64_t(vid) * 3 + pb_]), va.voxel_size);
+        const double sp0 = xsub(xadd(lo0, va.voxel_size), lo0);
+        const double sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
+        if (lane < 2 * mm) {
+            const int which = lane >= mm, r = lane - which * mm;
+            GC[lane] = xadd(which ? lo1 : lo0, xdiv(xmul(double(r) + 0.5, which ? sp1 : sp0), double(mm)));
+        }
+        __syncwarp();
+        // ---- separable tables (SE), transposed: lane = (table, training row)
+        if (kind == VX_KERNEL_SE) {
+            for (int e = lane; e < 2 * NMAX; e += 32) {
+                const int which = e / NMAX, i = e - which * NMAX;
+                double* T = (which ? EB : EA) + i;
+                if (i < n) {
+                    const double xi = X[2 * i + which];
+                    for (int r = 0; r < mm; ++r) {
+                        const double d = xsub(xi, GC[which * mm + r]);
+                        T[r * NMAX] = exp(xmul(-lam, xmul(d, d)));
+                    }
+                } else {
+                    for (int r = 0; r < mm; ++r) T[r * NMAX] = 0.0;
+                }
+            }
+        }
+
+        // ---- A = K + diag(noise), right-looking Cholesky in registers, one
+        //      jitter retry (gpr.py:184-194)
+        bool ok = false;
+        for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+            const double jit = attempt ? va.jitter : 0.0;
+            const int ntri = n * (n - 1) / 2;
+            for (int e = lane; e < ntri; e += 32) {
+                const int ij = TRI[e];
+                const int i = ij & 0xff, j = ij >> 8;
+                L[j * LD + i] = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
+            }
+            double dg = 1.0;                      // padding rows: identity
+            if (lane < n) {
+                dg = xadd(1.0, NZ[lane]);         // K_ii = exp(-lam*0) = 1, + noise
+                if (jit != 0.0) dg = xadd(dg, jit);
+            }
+            __syncwarp();
+            double a[NMAX];
+#pragma unroll
+            for (int k = 0; k < NMAX; ++k) {
+                double v = 0.0;
+                if (k == lane) v = dg;
+                else if (k < lane && lane < n) v = L[k * LD + lane];
+                a[k] = v;
+            }
+            __syncwarp();
+            ok = true;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) {
+                if (j >= n) break;
+                const double piv = __shfl_sync(FULL, a[j], j);
+                if (!(piv > 0.0)) {               // dpotrf: pivot <= 0 or NaN
+                    ok = false;
+                    break;
+                }
+                const double inv = rsqrt(piv);    // dpotf2 scales by 1/ajj
+                const double l = (lane == j) ? piv * inv : a[j] * inv;
+                a[j] = l;
+                if (lane < NMAX) L[j * LD + lane] = l;   // rows < j: unused upper entries
+                if (lane == 0) INV[j] = inv;
+                __syncwarp();
+                if (j + 1 < NMAX) {
+                    const double* Lj = L + j * LD;
+                    int k = j + 1;
+                    if (k & 1) {
+                        a[k] = fma(-l, Lj[k], a[k]);
+                        ++k;
+                    }
+#pragma unroll
+                    for (; k + 1 < NMAX; k += 2) {
+                        const double2 lk = *reinterpret_cast<const double2*>(Lj + k);
+                        a[k] = fma(-l, lk.x, a[k]);
+                        a[k + 1] = fma(-l, lk.y, a[k + 1]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (!ok) {
+            if (lane == 0) {
+                va.cand_status[s] = VX_ST_CHOL_FAIL;
+                const uint8_t st = va.state[vid];
+                va.cand_before[s] = st;
+                va.cand_after[s] = st;
+            }
+            __syncwarp();
+            continue;
+        }
+
+        // ---- L^-1, lane c = column c (rows >= n and columns >= n stay zero)
+        {
+            double x[NMAX];
+#pragma unroll
+            for (int r = 0; r < NMAX; ++r) {
+                double v = 0.0;
+                if (r < n) {
+                    double acc = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+                    for (int k = 0; k < r; ++k) acc = fma(-L[k * LD + r], x[k], acc);
+                    v = (r < lane) ? 0.0 : acc * INV[r];
+                }
+                x[r] = v;
+            }
+            __syncwarp();
+            if (lane < NMAX) {
+#pragma unroll
+                for (int r = 0; r < NMAX; ++r) L[r * LD + lane] = x[r];   // row-major L^-1
+            }
+            __syncwarp();
+        }
+        double bf[NA];                 // B = L^-T fragments: block (cb, s), s <= 2 cb + 1
+        {
+            int t = 0;
+#pragma unroll
+            for (int cb = 0; cb < NRB; ++cb)
+#pragma unroll
+                for (int s2 = 0; s2 < 2 * cb + 2; ++s2) bf[t++] = L[(8 * cb + g) * LD + 4 * s2 + tig];
+        }
+
+        // ---- W^T = [f | K*]^T L^-T by tiles of 8 right-hand sides
+        double zr[NRB][2];
+        for (int ct = 0; ct < ntiles; ++ct) {
+            const int col = 8 * ct + g;              // accumulator row = right-hand side
+            const int ri = QRI[col], si = QSI[col];
+            double af[NKS];
+            if (kind == VX_KERNEL_SE) {
+                const double* pA = ri >= 0 ? EA + ri * NMAX : (col == 0 ? F : ZERO);
+                const double* pB = si >= 0 ? EB + si * NMAX : ONE;
+#pragma unroll
+                for (int s2 = 0; s2 < NKS; ++s2) af[s2] = pA[4 * s2 + tig] * pB[4 * s2 + tig];
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 < NKS; ++s2) {
+                    const int row = 4 * s2 + tig;
+                    double v = 0.0;
+                    if (ri >= 0) {
+                        if (row < n) v = kernel_value(kind, lam, dist2_exact(X[2 * row], X[2 * row + 1],
+                                                                             GC[ri], GC[mm + si]));
+                    } else if (col == 0) {
+                        v = F[row];
+                    }
+                    af[s2] = v;
+                }
+            }
+            double c[NRB][2];
+            {
+                int t = 0;
+#pragma unroll
+                for (int cb = 0; cb < NRB; ++cb) {
+                    c[cb][0] = c[cb][1] = 0.0;
+#pragma unroll
+                    for (int s2 = 0; s2 < 2 * cb + 2; ++s2) dmma_acc(c[cb][0], c[cb][1], af[s2], bf[t++]);
+                }
+            }
+            if (ct == 0) {
+                // row 0 of tile 0 is z^T = (L^-1 f)^T: lanes 0..3 hold z(8 cb + 2 tig + e)
+#pragma unroll
+                for (int cb = 0; cb < NRB; ++cb) {
+                    zr[cb][0] = __shfl_sync(FULL, c[cb][0], tig);
+                    zr[cb][1] = __shfl_sync(FULL, c[cb][1], tig);
+                }
+            }
+            double ss = 0.0, mu = 0.0;
+#pragma unroll
+            for (int cb = 0; cb < NRB; ++cb) {
+                ss = fma(c[cb][0], c[cb][0], ss);
+                ss = fma(c[cb][1], c[cb][1], ss);
+                mu = fma(c[cb][0], zr[cb][0], mu);
+                mu = fma(c[cb][1], zr[cb][1], mu);
+            }
+            ss += __shfl_xor_sync(FULL, ss, 1);
+            mu += __shfl_xor_sync(FULL, mu, 1);
+            ss += __shfl_xor_sync(FULL, ss, 2);
+            mu += __shfl_xor_sync(FULL, mu, 2);
+            if (tig == 0 && col >= 1 && col < ncols) {
+                const double var = 1.0 - ss;
+                MU[col - 1] = xadd(mu, mean_f);
+                VAR[col - 1] = var < 0.0 ? 0.0 : var;      // np.clip(., 0, None)
+            }
+        }
+
+        // ---- nearest training point in the parameter plane (gpr.py:304-305), colours
+        int* BI = reinterpret_cast<int*>(base + lay.BI);
+        for (int q = lane; q < m; q += 32) {
+            const double g0 = GC[QRI[q + 1]], g1 = GC[mm + QSI[q + 1]];
+            double best = INFINITY;
+            int bi = 0;
+            for (int i = 0; i < n; ++i) {
+                const double d2 = dist2_exact(g0, g1, X[2 * i], X[2 * i + 1]);
+                if (d2 < best) { best = d2; bi = i; }
+            }
+            BI[q] = bi;
+        }
+        __syncwarp();
+        double* COL = base + lay.COL;
+        // read phase: colours may come from the previous prediction of this voxel
+        for (int q = lane; q < m; q += 32) {
+            const int bi = BI[q];
+            const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
+                                        : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
+            COL[q * 3] = cs[0];
+            COL[q * 3 + 1] = cs[1];
+            COL[q * 3 + 2] = cs[2];
+        }
+        __syncwarp();
+        double* oxyz = va.pred_xyz + int64_t(slot) * m * 3;
+        double* orgb = va.pred_rgb + int64_t(slot) * m * 3;
+        double* ovar = va.pred_var + int64_t(slot) * m;
+        for (int q = lane; q < m; q += 32) {
+            // assemble_points (gpr.py:89-97) with selects (no local-memory array)
+            const double pv = MU[q], p0 = GC[QRI[q + 1]], p1 = GC[mm + QSI[q + 1]];
+            oxyz[q * 3] = axis == 0 ? pv : (pa_ == 0 ? p0 : p1);
+            oxyz[q * 3 + 1] = axis == 1 ? pv : (pa_ == 1 ? p0 : p1);
+            oxyz[q * 3 + 2] = axis == 2 ? pv : (pa_ == 2 ? p0 : p1);
+            orgb[q * 3] = COL[q * 3];
+            orgb[q * 3 + 1] = COL[q * 3 + 1];
+            orgb[q * 3 + 2] = COL[q * 3 + 2];
+            ovar[q] = VAR[q];
+        }
+        const double mv = xdiv(warp_pairwise_sum(VAR, m), double(m));
+        if (lane == 0) {
+            const uint8_t before = va.state[vid];
+            const uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
+            va.state[vid] = after;
+            va.value_axis[vid] = int8_t(axis);
+            va.has_pred[vid] = 1;
+            va.cand_status[s] = VX_ST_OK;
+            va.cand_before[s] = before;
+            va.cand_after[s] = after;
+        }
+        __syncwarp();
+    }
+}
+
 // Packed block-column storage of the lower triangle: block column kb (columns
 // 8kb..8kb+7) holds rows 8kb..n8-1 column-major with leading dimension
 // ldb = rows + (4 or 12) so that ldb = 4 (mod 16) doubles and the four
@@ -2291,6 +2636,28 @@ static int launch_warp(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     return VX_OK;
 }
 
+template <int NMAX>
+static int launch_wdmma(const VoxelSolveArgs& va, int mm, cudaStream_t s) {
+    if (va.num_items <= 0) return VX_OK;
+    const WarpLayout lay(NMAX, mm, va.M, true);
+    const int ntiles = (va.M + 1 + 7) / 8;
+    constexpr int wpb = 4;
+    const size_t smem = size_t(lay.total) * sizeof(double) * wpb + 2 * NMAX * sizeof(double) +
+                        (size_t(ntiles) * 16 + NMAX * (NMAX - 1) / 2 + 1) * sizeof(int);
+    auto kfn = gpr_wdmma_kernel<NMAX>;
+    VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 32 * wpb, smem));
+    if (per_sm < 1) per_sm = 1;
+    int blocks = (va.num_items + wpb - 1) / wpb;
+    const int cap = sm_count() * per_sm;
+    if (blocks > cap) blocks = cap;
+    kfn<<<blocks, 32 * wpb, smem, s>>>(va, va.M, mm);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
 template <bool VOXEL>
 static int launch_generic(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int n_max,
                           int m_max, DevBuf& work, cudaStream_t s) {
@@ -2339,15 +2706,13 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         return VX_E_INPUT;
     }
     switch (bucket) {
-        case 0: return launch_warp<16, true>(a, none, a.num_items, a.M, mm, s);
-        case 1: return launch_warp<24, true>(a, none, a.num_items, a.M, mm, s);
-        case 5: return launch_warp<32, true>(a, none, a.num_items, a.M, mm, s);
+        case 0: return launch_wdmma<16>(a, mm, s);
+        case 1: return launch_wdmma<24>(a, mm, s);
+        case 5: return launch_wdmma<32>(a, mm, s);
         case 2:   // 32 < n <= 64: two 6-warp CTAs per SM, W streamed through L2
             return launch_big<6, true>(a, none, a.num_items, max_n < 64 ? max_n : 64, a.M, mm, work, s);
-            return launch_warp<64, true>(a, none, a.num_items, a.M, mm, s);
         case 6:   // 64 < n <= 96: same, measured faster than the register-resident tile kernel
             return launch_big<6, true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
-            return launch_cta<true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
         case 7:   // 128 < n <= 160
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n < 160 ? max_n : 160,
                                                            a.M, mm, work, s);
@@ -2355,7 +2720,6 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 3:   // 96 < n <= 128: register-resident DMMA tile kernel
             if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
             return launch_big<12, true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
-            return launch_cta<true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
         default:
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n, a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
