@@ -1592,11 +1592,10 @@ gpr_wdmma_kernel(VoxelSolveArgs va, int mmax, int mm) {
 
 // Packed block-column storage of the lower triangle: block column kb (columns
 // 8kb..8kb+7) holds rows 8kb..n8-1 column-major with leading dimension
-// ldb = rows + (4 or 12) so that ldb = 4 (mod 16) doubles and the four
-// columns of a DMMA fragment load land on disjoint bank pairs.
+// ldb = rows + 4 (rows a multiple of 8, so ldb = 4 or 12 mod 16 doubles): the
+// four columns of a DMMA fragment load land on disjoint banks per half-warp.
 __host__ __device__ inline int tile_ldb(int n8, int kb) {
-    const int rows = n8 - 8 * kb;
-    return rows + ((rows & 15) ? 12 : 4);
+    return n8 - 8 * kb + 4;
 }
 __host__ __device__ inline int tile_packed(int n8) {
     int t = 0;
@@ -1611,8 +1610,8 @@ struct TileLayout {
         int o = 0;
         L = o; o += tile_packed(N8);
         CO = o; o += N8 / 2 + 1;        // int32 column offsets: L(i, j) = L[CO[j] + i]
-        LINV = o; o += N8 * 8;          // inverses of the 8x8 diagonal blocks, row-major
         LDG = o; o += N8 * 8;           // factored 8x8 diagonal blocks, row-major
+        LINV = LDG;                     // then their inverses, in place
         X = o; o += 2 * N8;
         F = o; o += N8;
         NZ = o; o += N8;
@@ -1636,7 +1635,7 @@ struct TileLayout {
 };
 
 template <int NRB, int CTW, int NW, bool VOXEL>
-__global__ void __launch_bounds__(NW * 32, 1) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
+__global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
                                                            int mmax, int mm) {
     extern __shared__ __align__(16) double smem[];
     constexpr int N8 = NRB * 8;
@@ -1865,18 +1864,25 @@ __global__ void __launch_bounds__(NW * 32, 1) gpr_tile_kernel(VoxelSolveArgs va,
         }
         // inverses of the diagonal blocks (thread = (block, column)): L_kk x = e_c
         double* LINV = smem + lay.LINV;
-        for (int t = tid; t < nrb * 8; t += NT) {
+        // (LINV overlays LDG: every block is read before any thread overwrites it)
+        for (int t0 = 0; t0 < nrb * 8; t0 += NT) {
+            const int t = t0 + tid;
             const int kb = t >> 3, c = t & 7, b0 = kb * 8;
             double x[8];
+            if (t < nrb * 8) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                double v = (r == c) ? 1.0 : 0.0;
+                for (int r = 0; r < 8; ++r) {
+                    double v = (r == c) ? 1.0 : 0.0;
 #pragma unroll
-                for (int k = 0; k < r; ++k) v = fma(-LDG[(b0 + r) * 8 + k], x[k], v);
-                x[r] = (r < c) ? 0.0 : v * INV[b0 + r];
+                    for (int k = 0; k < r; ++k) v = fma(-LDG[(b0 + r) * 8 + k], x[k], v);
+                    x[r] = (r < c) ? 0.0 : v * INV[b0 + r];
+                }
             }
+            __syncthreads();
+            if (t < nrb * 8) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) LINV[(b0 + r) * 8 + c] = x[r];
+                for (int r = 0; r < 8; ++r) LINV[(b0 + r) * 8 + c] = x[r];
+            }
         }
         __syncthreads();
 
@@ -2330,18 +2336,25 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
         }
         // inverses of the diagonal blocks (thread = (block, column)): L_kk x = e_c
         double* LINV = smem + lay.LINV;
-        for (int t = tid; t < nrb * 8; t += NT) {
+        // (LINV overlays LDG: every block is read before any thread overwrites it)
+        for (int t0 = 0; t0 < nrb * 8; t0 += NT) {
+            const int t = t0 + tid;
             const int kb = t >> 3, c = t & 7, b0 = kb * 8;
             double x[8];
+            if (t < nrb * 8) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                double v = (r == c) ? 1.0 : 0.0;
+                for (int r = 0; r < 8; ++r) {
+                    double v = (r == c) ? 1.0 : 0.0;
 #pragma unroll
-                for (int k = 0; k < r; ++k) v = fma(-LDG[(b0 + r) * 8 + k], x[k], v);
-                x[r] = (r < c) ? 0.0 : v * INV[b0 + r];
+                    for (int k = 0; k < r; ++k) v = fma(-LDG[(b0 + r) * 8 + k], x[k], v);
+                    x[r] = (r < c) ? 0.0 : v * INV[b0 + r];
+                }
             }
+            __syncthreads();
+            if (t < nrb * 8) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) LINV[(b0 + r) * 8 + c] = x[r];
+                for (int r = 0; r < 8; ++r) LINV[(b0 + r) * 8 + c] = x[r];
+            }
         }
         __syncthreads();
 
@@ -2709,16 +2722,18 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 0: return launch_wdmma<16>(a, mm, s);
         case 1: return launch_wdmma<24>(a, mm, s);
         case 5: return launch_wdmma<32>(a, mm, s);
-        case 2:   // 32 < n <= 64: two 6-warp CTAs per SM, W streamed through L2
+        case 2:   // 32 < n <= 64: two 6-warp CTAs per SM, right-hand sides in registers
+            if (a.M + 1 <= 96) return launch_tile<8, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
             return launch_big<6, true>(a, none, a.num_items, max_n < 64 ? max_n : 64, a.M, mm, work, s);
-        case 6:   // 64 < n <= 96: same, measured faster than the register-resident tile kernel
+        case 6:   // 64 < n <= 96: same kernel as n <= 128 (rows beyond n skipped)
+            if (a.M + 1 <= 96) return launch_tile<16, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
             return launch_big<6, true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
         case 7:   // 128 < n <= 160
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n < 160 ? max_n : 160,
                                                            a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 160 ? max_n : 160, a.M, mm, work, s);
         case 3:   // 96 < n <= 128: register-resident DMMA tile kernel
-            if (a.M + 1 <= 96) return launch_tile<16, 1, 12, true>(a, none, a.num_items, a.M, mm, s);
+            if (a.M + 1 <= 96) return launch_tile<16, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
             return launch_big<12, true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
         default:
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n, a.M, mm, work, s);
@@ -2737,9 +2752,9 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
         if (bucket == 0) return launch_warp<16, false>(none, pa, count, max_m, 1, s);
         if (bucket == 1) return launch_warp<24, false>(none, pa, count, max_m, 1, s);
         if (bucket == 5) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 2) return launch_tile<8, 3, 4, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 6) return launch_tile<16, 1, 12, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 3) return launch_tile<16, 1, 12, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 2) return launch_tile<8, 2, 6, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 6) return launch_tile<16, 2, 6, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 3) return launch_tile<16, 2, 6, false>(none, pa, count, max_m, 1, s);
 
         return launch_big<12, false>(none, pa, count, max_n, max_m, 1, work, s);
     }
