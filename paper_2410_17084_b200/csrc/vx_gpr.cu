@@ -1604,7 +1604,7 @@ __host__ __device__ inline int tile_packed(int n8) {
 }
 
 struct TileLayout {
-    int L, CO, LINV, LDG, X, F, NZ, INV, Z, EA, EB, MU, VAR, BI, COL, FLAG, W, total;
+    int L, CO, LINV, LDG, X, F, NZ, INV, Z, EA, EB, MU, VAR, COL, FLAG, GC, QT, W, total;
     __host__ __device__ TileLayout(int N8, int mm, int mcols, int mmax, bool voxel,
                                    bool with_w = false) {
         int o = 0;
@@ -1617,7 +1617,7 @@ struct TileLayout {
         NZ = o; o += N8;
         INV = o; o += N8;
         Z = o; o += N8;
-        EA = EB = MU = VAR = BI = COL = o;
+        EA = EB = COL = o;
         if (voxel) {
             EA = o; o += N8 * mm;
             EB = o; o += N8 * mm;
@@ -1625,14 +1625,173 @@ struct TileLayout {
         }
         MU = o; o += mcols;
         VAR = o; o += mcols;
-        BI = o; o += mcols;
         FLAG = o; o += 2;
+        GC = o; o += 2 * MAX_MM;        // grid coordinates of both parameter axes
+        QT = o; o += mcols;             // int32 (ri, si) of column c = q + 1
         o = (o + 1) & ~1;
         W = o;
         if (with_w) o += N8 * mcols;    // row-major right-hand-side block (big kernel)
         total = (o + 1) & ~1;
     }
 };
+
+// ---------------------------------------------------------------------------
+// CTA helpers shared by the DMMA tile and big kernels (voxel mode)
+// ---------------------------------------------------------------------------
+struct VoxelCtx {
+    int s, vid, n, cnt, slot, axis;
+    int64_t off;
+    double mean_f, lo0, lo1, sp0, sp1;
+};
+
+// work item -> staged training set raw ∪ pseudo (voxel_map.py:196-200) split
+// by the value axis: X (n, 2) parameter coordinates, F = f - mean(f)
+// (gpr.py:291-294), NZ per-point noise; rows [n, npad) are zero.  Also the
+// voxel's parameter-plane origin and extent (gpr.py:262-266).
+__device__ __forceinline__ VoxelCtx team_stage_voxel(const VoxelSolveArgs& va, int it, double* X,
+                                                     double* F, double* NZ, int npad, int tid,
+                                                     int nt) {
+    VoxelCtx c;
+    c.s = va.items[it];
+    c.vid = va.cand_voxel[c.s];
+    c.n = va.cand_n[c.s];
+    c.cnt = va.raw_count[c.vid];
+    c.off = va.raw_offset[c.vid];
+    c.slot = va.pred_slot[c.vid];
+    c.axis = va.cand_axis[c.s];
+    c.mean_f = va.cand_meanf[c.s];
+    const int pa_ = param_axis_a(c.axis), pb_ = param_axis_b(c.axis);
+    for (int r = tid; r < npad; r += nt) {
+        if (r < c.n) {
+            const double* p = train_point(va, r, c.cnt, c.off, c.slot);
+            X[2 * r] = p[pa_];
+            X[2 * r + 1] = p[pb_];
+            F[r] = xsub(p[c.axis], c.mean_f);
+            NZ[r] = r < c.cnt ? va.sensor_var : va.pred_var[int64_t(c.slot) * va.M + (r - c.cnt)];
+        } else {
+            X[2 * r] = X[2 * r + 1] = F[r] = NZ[r] = 0.0;
+        }
+    }
+    c.lo0 = xmul(double(va.keys[int64_t(c.vid) * 3 + pa_]), va.voxel_size);
+    c.lo1 = xmul(double(va.keys[int64_t(c.vid) * 3 + pb_]), va.voxel_size);
+    c.sp0 = xsub(xadd(c.lo0, va.voxel_size), c.lo0);
+    c.sp1 = xsub(xadd(c.lo1, va.voxel_size), c.lo1);
+    return c;
+}
+
+// grid coordinates c_r = lo + ((r + 0.5) * (hi - lo)) / m (gpr.py:104-120):
+// GC[r] on the first parameter axis, GC[mm + r] on the second
+__device__ __forceinline__ void team_grid_coords(double* GC, const VoxelCtx& c, int mm, int tid) {
+    if (tid < 2 * mm) {
+        const int which = tid >= mm, r = tid - which * mm;
+        GC[tid] = xadd(which ? c.lo1 : c.lo0, xdiv(xmul(double(r) + 0.5, which ? c.sp1 : c.sp0), double(mm)));
+    }
+}
+
+// separable SE tables T[i * mm + r] = exp(-lam (x_i - c_r)^2), rows i < n:
+// k*(x_i, (c_ri, c_si)) = EA[i][ri] * EB[i][si]
+__device__ __forceinline__ void team_se_tables(double* EA, double* EB, const double* X,
+                                               const double* GC, int n, int mm, double lam,
+                                               int tid, int nt) {
+    for (int e = tid; e < 2 * n; e += nt) {
+        const int which = e >= n, i = e - which * n;
+        const double xi = X[2 * i + which];
+        const double* G = GC + which * mm;
+        double* T = (which ? EB : EA) + i * mm;
+        for (int r = 0; r < mm; ++r) {
+            const double d = xsub(xi, G[r]);
+            T[r] = exp(xmul(-lam, xmul(d, d)));
+        }
+    }
+}
+
+// column c of [f | K*] -> grid indices (ri, si) of query q = c - 1, packed
+// ri | si << 16 (-1 for c == 0 and padding columns); query order is
+// (sub-row, sub-col, fine-row, fine-col) as make_mesh_grid (gpr.py:104-120)
+__device__ __forceinline__ void team_query_table(int* QT, const VoxelSolveArgs& va, int ncols_pad,
+                                                 int tid, int nt) {
+    for (int c = tid; c < ncols_pad; c += nt) {
+        int v = -1;
+        if (c >= 1 && c <= va.M) {
+            const int q = c - 1;
+            const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
+            const int sr = q / (ns * nr2);
+            const int rem = q - sr * ns * nr2;
+            const int sc = rem / nr2;
+            const int rem2 = rem - sc * nr2;
+            const int fr = rem2 / nr, fc = rem2 - fr * nr;
+            v = (sr * nr + fr) | ((sc * nr + fc) << 16);
+        }
+        QT[c] = v;
+    }
+}
+
+// Voxel epilogue (gpr.py:303-310, voxel_map.py:242-261): nearest training
+// point in the parameter plane (first index on ties) with two threads per
+// query, colour gather (all reads before any write: the colour source may be
+// this voxel's previous prediction), assemble_points, clipped variances and
+// the lifecycle update.  MU / VAR are indexed by column c = q + 1.
+__device__ void team_voxel_epilogue(const VoxelSolveArgs& va, const VoxelCtx& c, const double* X,
+                                    const double* GC, const int* QT, int mm, const double* MU,
+                                    const double* VAR, double* COL, int tid, int nt) {
+    const int m = va.M;
+    const int h = (c.n + 1) >> 1;
+    for (int t0 = 0; t0 < 2 * m; t0 += nt) {       // uniform trip count: pairs are lanes 2k, 2k+1
+        const int t = t0 + tid, q = t >> 1, half = t & 1;
+        double best = INFINITY;
+        int bi = 0x7fffffff;
+        if (q < m) {
+            const int qt = QT[q + 1];
+            const double g0 = GC[qt & 0xffff], g1 = GC[mm + (qt >> 16)];
+            const int lo = half ? h : 0, hi = half ? c.n : h;
+            for (int i = lo; i < hi; ++i) {
+                const double d2 = dist2_exact(g0, g1, X[2 * i], X[2 * i + 1]);
+                if (d2 < best) { best = d2; bi = i; }
+            }
+        }
+        const double ob = __shfl_xor_sync(FULL, best, 1);
+        const int oi = __shfl_xor_sync(FULL, bi, 1);
+        if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        if (q < m && half == 0) {
+            if (bi >= c.n) bi = 0;
+            const double* cs = bi < c.cnt ? va.raw_rgb + (c.off + bi) * 3
+                                          : va.pred_rgb + (int64_t(c.slot) * m + (bi - c.cnt)) * 3;
+            COL[q * 3] = cs[0];
+            COL[q * 3 + 1] = cs[1];
+            COL[q * 3 + 2] = cs[2];
+        }
+    }
+    __syncthreads();
+    const int pa_ = param_axis_a(c.axis);
+    double* oxyz = va.pred_xyz + int64_t(c.slot) * m * 3;
+    double* orgb = va.pred_rgb + int64_t(c.slot) * m * 3;
+    double* ovar = va.pred_var + int64_t(c.slot) * m;
+    for (int q = tid; q < m; q += nt) {
+        // assemble_points (gpr.py:89-97)
+        const int qt = QT[q + 1];
+        const double pv = MU[q + 1], p0 = GC[qt & 0xffff], p1 = GC[mm + (qt >> 16)];
+        oxyz[q * 3] = c.axis == 0 ? pv : (pa_ == 0 ? p0 : p1);
+        oxyz[q * 3 + 1] = c.axis == 1 ? pv : (pa_ == 1 ? p0 : p1);
+        oxyz[q * 3 + 2] = c.axis == 2 ? pv : (pa_ == 2 ? p0 : p1);
+        orgb[q * 3] = COL[q * 3];
+        orgb[q * 3 + 1] = COL[q * 3 + 1];
+        orgb[q * 3 + 2] = COL[q * 3 + 2];
+        ovar[q] = VAR[q + 1];
+    }
+    if (tid < 32) {
+        const double mv = xdiv(warp_pairwise_sum(VAR + 1, m), double(m));
+        if (tid == 0) {
+            const uint8_t before = va.state[c.vid];
+            const uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
+            va.state[c.vid] = after;
+            va.value_axis[c.vid] = int8_t(c.axis);
+            va.has_pred[c.vid] = 1;
+            va.cand_status[c.s] = VX_ST_OK;
+            va.cand_before[c.s] = before;
+            va.cand_after[c.s] = after;
+        }
+    }
+}
 
 template <int NRB, int CTW, int NW, bool VOXEL>
 __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
@@ -1653,60 +1812,36 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, tig = lane & 3;
     const int num_items = VOXEL ? va.num_items : pa.num_items;
+    double* GC = smem + lay.GC;
+    int* QT = reinterpret_cast<int*>(smem + lay.QT);
+    if constexpr (VOXEL) {
+        team_query_table(QT, va, PCOLS, tid, NT);
+        __syncthreads();
+    }
 
     for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
         int n, m, s, vid = 0, cnt = 0, slot = 0, axis = 2;
         int64_t off = 0, xo = 0, qo = 0;
         double lam, jitter, mean_f = 0.0;
         int kind;
-        double lo0 = 0, lo1 = 0, sp0 = 0, sp1 = 0;
+        VoxelCtx vc{};
         if constexpr (VOXEL) {
-            s = va.items[it];
-            vid = va.cand_voxel[s];
-            n = va.cand_n[s];
-            cnt = va.raw_count[vid];
-            off = va.raw_offset[vid];
-            slot = va.pred_slot[vid];
+            vc = team_stage_voxel(va, it, X, F, NZ, N8, tid, NT);
+            s = vc.s;
+            vid = vc.vid;
+            n = vc.n;
+            cnt = vc.cnt;
+            off = vc.off;
+            slot = vc.slot;
+            axis = vc.axis;
+            mean_f = vc.mean_f;
             m = va.M;
             lam = va.lam;
             jitter = va.jitter;
             kind = va.kernel;
-            axis = va.cand_axis[s];
-            mean_f = va.cand_meanf[s];
-            const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
-            for (int r = tid; r < N8; r += NT) {
-                if (r < n) {
-                    const double* p = train_point(va, r, cnt, off, slot);
-                    X[2 * r] = p[pa_];
-                    X[2 * r + 1] = p[pb_];
-                    F[r] = xsub(p[axis], mean_f);
-                    NZ[r] = r < cnt ? va.sensor_var : va.pred_var[int64_t(slot) * m + (r - cnt)];
-                } else {
-                    X[2 * r] = X[2 * r + 1] = F[r] = NZ[r] = 0.0;
-                }
-            }
-            lo0 = xmul(double(va.keys[int64_t(vid) * 3 + pa_]), va.voxel_size);
-            lo1 = xmul(double(va.keys[int64_t(vid) * 3 + pb_]), va.voxel_size);
-            sp0 = xsub(xadd(lo0, va.voxel_size), lo0);
-            sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
+            team_grid_coords(GC, vc, mm, tid);
             __syncthreads();
-            if (kind == VX_KERNEL_SE) {
-                double* EA = smem + lay.EA;
-                double* EB = smem + lay.EB;
-                for (int e = tid; e < 2 * N8 * mm; e += NT) {
-                    const int which = e >= N8 * mm;
-                    const int rem = e - which * N8 * mm;
-                    const int i = rem / mm, r = rem - i * mm;
-                    double v = 0.0;
-                    if (i < n) {
-                        const double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
-                        const double gg = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
-                        const double d = xsub(X[2 * i + which], gg);
-                        v = exp(xmul(-lam, xmul(d, d)));
-                    }
-                    (which ? EB : EA)[i * mm + r] = v;
-                }
-            }
+            if (kind == VX_KERNEL_SE) team_se_tables(smem + lay.EA, smem + lay.EB, X, GC, n, mm, lam, tid, NT);
         } else {
             s = pa.items[it];
             xo = pa.x_off[s];
@@ -1903,16 +2038,11 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
                     double g0 = 0, g1 = 0;
                     if (c > 0 && c < ncols) {
                         if constexpr (VOXEL) {
-                            const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
-                            const int sr = q / (ns * nr2);
-                            const int rem = q - sr * ns * nr2;
-                            const int sc = rem / nr2;
-                            const int rem2 = rem - sc * nr2;
-                            const int fr = rem2 / nr, fc = rem2 - fr * nr;
-                            ri = sr * nr + fr;
-                            si = sc * nr + fc;
-                            g0 = xadd(lo0, xdiv(xmul(double(ri) + 0.5, sp0), double(mm)));
-                            g1 = xadd(lo1, xdiv(xmul(double(si) + 0.5, sp1), double(mm)));
+                            const int qt = QT[c];
+                            ri = qt & 0xffff;
+                            si = qt >> 16;
+                            g0 = GC[ri];
+                            g1 = GC[mm + si];
                         } else {
                             g0 = pa.xs[(qo + q) * 2];
                             g1 = pa.xs[(qo + q) * 2 + 1];
@@ -2029,66 +2159,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
             if constexpr (VOXEL) {
                 // voxel mode: m + 1 <= PCOLS (asserted by the launcher), one pass
                 __syncthreads();
-                double* COL = smem + lay.COL;
-                int* BI = reinterpret_cast<int*>(smem + lay.BI);
-                for (int q = tid; q < m; q += NT) {
-                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
-                    const int sr = q / (ns * nr2);
-                    const int rem = q - sr * ns * nr2;
-                    const int sc = rem / nr2;
-                    const int rem2 = rem - sc * nr2;
-                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
-                    const double g0 = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
-                    const double g1 = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
-                    double best = INFINITY;
-                    int bi = 0;
-                    for (int t = 0; t < n; ++t) {
-                        const double d2 = dist2_exact(g0, g1, X[2 * t], X[2 * t + 1]);
-                        if (d2 < best) { best = d2; bi = t; }
-                    }
-                    BI[q] = bi;
-                    const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
-                                                : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
-                    COL[q * 3] = cs[0];
-                    COL[q * 3 + 1] = cs[1];
-                    COL[q * 3 + 2] = cs[2];
-                }
-                __syncthreads();
-                const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
-                double* oxyz = va.pred_xyz + int64_t(slot) * m * 3;
-                double* orgb = va.pred_rgb + int64_t(slot) * m * 3;
-                double* ovar = va.pred_var + int64_t(slot) * m;
-                for (int q = tid; q < m; q += NT) {
-                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
-                    const int sr = q / (ns * nr2);
-                    const int rem = q - sr * ns * nr2;
-                    const int sc = rem / nr2;
-                    const int rem2 = rem - sc * nr2;
-                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
-                    double pos[3];
-                    pos[axis] = smem[lay.MU + q + 1];
-                    pos[pa_] = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
-                    pos[pb_] = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
-                    oxyz[q * 3] = pos[0];
-                    oxyz[q * 3 + 1] = pos[1];
-                    oxyz[q * 3 + 2] = pos[2];
-                    orgb[q * 3] = COL[q * 3];
-                    orgb[q * 3 + 1] = COL[q * 3 + 1];
-                    orgb[q * 3 + 2] = COL[q * 3 + 2];
-                    ovar[q] = smem[lay.VAR + q + 1];
-                }
-                if (tid == 0) {
-                    const double* V = smem + lay.VAR + 1;
-                    const double mv = xdiv(np_pairwise_sum([V](int i) { return V[i]; }, m), double(m));
-                    const uint8_t before = va.state[vid];
-                    const uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
-                    va.state[vid] = after;
-                    va.value_axis[vid] = int8_t(axis);
-                    va.has_pred[vid] = 1;
-                    va.cand_status[s] = VX_ST_OK;
-                    va.cand_before[s] = before;
-                    va.cand_after[s] = after;
-                }
+                team_voxel_epilogue(va, vc, X, GC, QT, mm, smem + lay.MU, smem + lay.VAR,
+                                    smem + lay.COL, tid, NT);
             }
             __syncthreads();
         }
@@ -2125,60 +2197,36 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, tig = lane & 3;
     const int num_items = VOXEL ? va.num_items : pa.num_items;
+    double* GC = smem + lay.GC;
+    int* QT = reinterpret_cast<int*>(smem + lay.QT);
+    if constexpr (VOXEL) {
+        team_query_table(QT, va, MC, tid, NT);
+        __syncthreads();
+    }
 
     for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
         int n, m, s, vid = 0, cnt = 0, slot = 0, axis = 2;
         int64_t off = 0, xo = 0, qo = 0;
         double lam, jitter, mean_f = 0.0;
         int kind;
-        double lo0 = 0, lo1 = 0, sp0 = 0, sp1 = 0;
+        VoxelCtx vc{};
         if constexpr (VOXEL) {
-            s = va.items[it];
-            vid = va.cand_voxel[s];
-            n = va.cand_n[s];
-            cnt = va.raw_count[vid];
-            off = va.raw_offset[vid];
-            slot = va.pred_slot[vid];
+            vc = team_stage_voxel(va, it, X, F, NZ, N8, tid, NT);
+            s = vc.s;
+            vid = vc.vid;
+            n = vc.n;
+            cnt = vc.cnt;
+            off = vc.off;
+            slot = vc.slot;
+            axis = vc.axis;
+            mean_f = vc.mean_f;
             m = va.M;
             lam = va.lam;
             jitter = va.jitter;
             kind = va.kernel;
-            axis = va.cand_axis[s];
-            mean_f = va.cand_meanf[s];
-            const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
-            for (int r = tid; r < N8; r += NT) {
-                if (r < n) {
-                    const double* p = train_point(va, r, cnt, off, slot);
-                    X[2 * r] = p[pa_];
-                    X[2 * r + 1] = p[pb_];
-                    F[r] = xsub(p[axis], mean_f);
-                    NZ[r] = r < cnt ? va.sensor_var : va.pred_var[int64_t(slot) * m + (r - cnt)];
-                } else {
-                    X[2 * r] = X[2 * r + 1] = F[r] = NZ[r] = 0.0;
-                }
-            }
-            lo0 = xmul(double(va.keys[int64_t(vid) * 3 + pa_]), va.voxel_size);
-            lo1 = xmul(double(va.keys[int64_t(vid) * 3 + pb_]), va.voxel_size);
-            sp0 = xsub(xadd(lo0, va.voxel_size), lo0);
-            sp1 = xsub(xadd(lo1, va.voxel_size), lo1);
+            team_grid_coords(GC, vc, mm, tid);
             __syncthreads();
-            if (kind == VX_KERNEL_SE) {
-                double* EA = smem + lay.EA;
-                double* EB = smem + lay.EB;
-                for (int e = tid; e < 2 * N8 * mm; e += NT) {
-                    const int which = e >= N8 * mm;
-                    const int rem = e - which * N8 * mm;
-                    const int i = rem / mm, r = rem - i * mm;
-                    double v = 0.0;
-                    if (i < n) {
-                        const double lo = which ? lo1 : lo0, sp = which ? sp1 : sp0;
-                        const double gg = xadd(lo, xdiv(xmul(double(r) + 0.5, sp), double(mm)));
-                        const double d = xsub(X[2 * i + which], gg);
-                        v = exp(xmul(-lam, xmul(d, d)));
-                    }
-                    (which ? EB : EA)[i * mm + r] = v;
-                }
-            }
+            if (kind == VX_KERNEL_SE) team_se_tables(smem + lay.EA, smem + lay.EB, X, GC, n, mm, lam, tid, NT);
         } else {
             s = pa.items[it];
             xo = pa.x_off[s];
@@ -2373,16 +2421,11 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
                 const int q = c - 1;
                 if (c > 0 && c < ncols) {
                     if constexpr (VOXEL) {
-                        const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
-                        const int sr = q / (ns * nr2);
-                        const int rem = q - sr * ns * nr2;
-                        const int sc = rem / nr2;
-                        const int rem2 = rem - sc * nr2;
-                        const int fr = rem2 / nr, fc = rem2 - fr * nr;
-                        ri[e] = sr * nr + fr;
-                        si[e] = sc * nr + fc;
-                        g0[e] = xadd(lo0, xdiv(xmul(double(ri[e]) + 0.5, sp0), double(mm)));
-                        g1[e] = xadd(lo1, xdiv(xmul(double(si[e]) + 0.5, sp1), double(mm)));
+                        const int qt = QT[c];
+                        ri[e] = qt & 0xffff;
+                        si[e] = qt >> 16;
+                        g0[e] = GC[ri[e]];
+                        g1[e] = GC[mm + si[e]];
                     } else {
                         g0[e] = pa.xs[(qo + q) * 2];
                         g1[e] = pa.xs[(qo + q) * 2 + 1];
@@ -2467,66 +2510,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
             if constexpr (VOXEL) {
                 // every pass has written MU / VAR (indexed by column): epilogue once
                 __syncthreads();
-                double* COL = smem + lay.COL;
-                int* BI = reinterpret_cast<int*>(smem + lay.BI);
-                for (int q = tid; q < m; q += NT) {
-                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
-                    const int sr = q / (ns * nr2);
-                    const int rem = q - sr * ns * nr2;
-                    const int sc = rem / nr2;
-                    const int rem2 = rem - sc * nr2;
-                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
-                    const double g0 = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
-                    const double g1 = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
-                    double best = INFINITY;
-                    int bi = 0;
-                    for (int t = 0; t < n; ++t) {
-                        const double d2 = dist2_exact(g0, g1, X[2 * t], X[2 * t + 1]);
-                        if (d2 < best) { best = d2; bi = t; }
-                    }
-                    BI[q] = bi;
-                    const double* cs = bi < cnt ? va.raw_rgb + (off + bi) * 3
-                                                : va.pred_rgb + (int64_t(slot) * m + (bi - cnt)) * 3;
-                    COL[q * 3] = cs[0];
-                    COL[q * 3 + 1] = cs[1];
-                    COL[q * 3 + 2] = cs[2];
-                }
-                __syncthreads();
-                const int pa_ = param_axis_a(axis), pb_ = param_axis_b(axis);
-                double* oxyz = va.pred_xyz + int64_t(slot) * m * 3;
-                double* orgb = va.pred_rgb + int64_t(slot) * m * 3;
-                double* ovar = va.pred_var + int64_t(slot) * m;
-                for (int q = tid; q < m; q += NT) {
-                    const int nr = va.n_r, ns = va.n_s, nr2 = nr * nr;
-                    const int sr = q / (ns * nr2);
-                    const int rem = q - sr * ns * nr2;
-                    const int sc = rem / nr2;
-                    const int rem2 = rem - sc * nr2;
-                    const int fr = rem2 / nr, fc = rem2 - fr * nr;
-                    double pos[3];
-                    pos[axis] = smem[lay.MU + q + 1];
-                    pos[pa_] = xadd(lo0, xdiv(xmul(double(sr * nr + fr) + 0.5, sp0), double(mm)));
-                    pos[pb_] = xadd(lo1, xdiv(xmul(double(sc * nr + fc) + 0.5, sp1), double(mm)));
-                    oxyz[q * 3] = pos[0];
-                    oxyz[q * 3 + 1] = pos[1];
-                    oxyz[q * 3 + 2] = pos[2];
-                    orgb[q * 3] = COL[q * 3];
-                    orgb[q * 3 + 1] = COL[q * 3 + 1];
-                    orgb[q * 3 + 2] = COL[q * 3 + 2];
-                    ovar[q] = smem[lay.VAR + q + 1];
-                }
-                if (tid == 0) {
-                    const double* V = smem + lay.VAR + 1;
-                    const double mv = xdiv(np_pairwise_sum([V](int i) { return V[i]; }, m), double(m));
-                    const uint8_t before = va.state[vid];
-                    const uint8_t after = mv <= va.eta ? VX_CONVERGED : VX_ACTIVE;
-                    va.state[vid] = after;
-                    va.value_axis[vid] = int8_t(axis);
-                    va.has_pred[vid] = 1;
-                    va.cand_status[s] = VX_ST_OK;
-                    va.cand_before[s] = before;
-                    va.cand_after[s] = after;
-                }
+                team_voxel_epilogue(va, vc, X, GC, QT, mm, smem + lay.MU, smem + lay.VAR,
+                                    smem + lay.COL, tid, NT);
             }
             __syncthreads();
         }
