@@ -1635,6 +1635,83 @@ struct TileLayout {
     }
 };
 
+// Cholesky update of the 8x8 tile (rows 8t.., panel columns jp..jp+7):
+// A -= L(rows, k_lo:k_hi) L(panel, k_lo:k_hi)^T with DMMA; k_lo, k_hi are
+// multiples of 8 and the two k-chunks of each block column feed separate
+// accumulators (half the dependent-DMMA chain); one CO lookup per block column.
+__device__ __forceinline__ void chol_tile_update(double* L, const int* CO, int n8, int t, int jp,
+                                                 int k_lo, int k_hi, int g, int tig) {
+    const int rb = t * 8;
+    double* p0 = L + CO[jp + 2 * tig] + rb + g;
+    double* p1 = L + CO[jp + 2 * tig + 1] + rb + g;
+    double c0 = *p0, c1 = *p1, d0 = 0.0, d1 = 0.0;
+    for (int k8 = k_lo; k8 < k_hi; k8 += 8) {
+        const double* col = L + CO[k8 + tig];
+        const int o4 = 4 * tile_ldb(n8, k8 >> 3);
+        dmma_acc(c0, c1, -col[rb + g], col[jp + g]);
+        dmma_acc(d0, d1, -col[o4 + rb + g], col[o4 + jp + g]);
+    }
+    *p0 = c0 + d0;
+    *p1 = c1 + d1;
+}
+
+// Step (b)+(c) of the panel Cholesky, run by each of `nft` threads: factor the
+// 8x8 diagonal block at j0 in registers (dpotf2 order: scale by 1/sqrt(ajj),
+// then the rank-1 update, gpr.py:187 cho_factor) - every thread redundantly,
+// so there is no shuffle or shared-memory hand-off on the critical path - then
+// solve this thread's row below the block, L(i, J) = A(i, J) L_JJ^-T, in the
+// same operation order as the column-oriented substitution.  Thread 0
+// publishes the factored block (LDG, row-major), 1/L_jj (INV) and the pivot
+// flag (0 when a pivot is <= 0 or NaN, the dpotrf failure rule).
+__device__ __forceinline__ void chol_diag_and_rows(double* L, const int* CO, double* LDG,
+                                                   double* INV, double* flag, int j0, int n8,
+                                                   int tid, int nft) {
+    double a[36];                                   // packed lower triangle, row-major
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) a[r * (r + 1) / 2 + c] = L[CO[j0 + c] + j0 + r];
+    double inv[8];
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const double piv = a[c * (c + 1) / 2 + c];
+        if (!(piv > 0.0)) ok = false;
+        inv[c] = rsqrt(piv);
+        a[c * (c + 1) / 2 + c] = piv * inv[c];
+#pragma unroll
+        for (int r = c + 1; r < 8; ++r) a[r * (r + 1) / 2 + c] *= inv[c];
+#pragma unroll
+        for (int r = c + 1; r < 8; ++r)
+#pragma unroll
+            for (int k = c + 1; k <= r; ++k)
+                a[r * (r + 1) / 2 + k] = fma(-a[r * (r + 1) / 2 + c], a[k * (k + 1) / 2 + c],
+                                             a[r * (r + 1) / 2 + k]);
+    }
+    if (tid == 0) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) LDG[(j0 + r) * 8 + k] = k <= r ? a[r * (r + 1) / 2 + k] : 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) INV[j0 + c] = inv[c];
+        *flag = ok ? 1.0 : 0.0;
+    }
+    for (int i = j0 + 8 + tid; i < n8; i += nft) {
+        double v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = L[CO[j0 + c] + i];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            v[c] *= inv[c];
+#pragma unroll
+            for (int k = c + 1; k < 8; ++k) v[k] = fma(-v[c], a[k * (k + 1) / 2 + c], v[k]);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) L[CO[j0 + c] + i] = v[c];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // CTA helpers shared by the DMMA tile and big kernels (voxel mode)
 // ---------------------------------------------------------------------------
@@ -1898,16 +1975,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
             ok = true;
             // DMMA update of one 8x8 row tile of panel `jp` with columns [k_lo, k_hi)
             auto tile_update = [&](int t, int jp, int k_lo, int k_hi) {
-                const int rb = t * 8;
-                double c0 = L[CO[jp + 2 * tig] + rb + g];
-                double c1 = L[CO[jp + 2 * tig + 1] + rb + g];
-                for (int k4 = k_lo; k4 < k_hi; k4 += 4) {
-                    const double a = -L[CO[k4 + tig] + rb + g];
-                    const double b = L[CO[k4 + tig] + jp + g];
-                    dmma_acc(c0, c1, a, b);
-                }
-                L[CO[jp + 2 * tig] + rb + g] = c0;
-                L[CO[jp + 2 * tig + 1] + rb + g] = c1;
+                chol_tile_update(L, CO, n8, t, jp, k_lo, k_hi, g, tig);
             };
             bool la_prev = false;   // look-ahead already applied columns < j0 - 8 to this panel
             for (int kb = 0; kb < nrb; ++kb) {
@@ -1919,13 +1987,11 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
                     for (int t = kb + warp; t < nrb; t += NW) tile_update(t, j0, klo, j0);
                     __syncthreads();
                 }
-                // (b) the warps that solve rows below this block (and warp 0, which
-                // publishes INV / LDG / the pivot flag) factor the 8x8 diagonal block
-                // redundantly (lane r holds row r).  Identical inputs give identical
-                // outputs, so the duplicate shared-memory stores are benign and no
-                // barrier separates the factorisation from the rows below.  The other
-                // warps meanwhile apply every final column (< j0) to the NEXT panel
-                // (look-ahead), hiding the serial factorisation behind the GEMM work.
+                // (b) every thread of the warps that own rows below this block (warp 0
+                // at least) factors the 8x8 diagonal block in its own registers and
+                // solves its row against it: no shuffles and no barrier between the
+                // two.  The other warps meanwhile apply every final column (< j0) to
+                // the NEXT panel (look-ahead), hiding the serial factorisation.
                 const int below = n8 - j0 - 8;
                 const int nfw = below > 32 ? (below + 31) / 32 : 1;
                 const bool la = (kb + 1 < nrb) && (NW > nfw) && j0 > 0;
@@ -1934,45 +2000,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
                         for (int t = kb + 1 + (warp - nfw); t < nrb; t += NW - nfw)
                             tile_update(t, j0 + 8, 0, j0);
                 } else {
-                    double d[8];
-                    const int r = lane & 7;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) d[k] = (k <= r) ? L[CO[j0 + k] + j0 + r] : 0.0;
-                    bool okw = true;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const double piv = __shfl_sync(FULL, d[c], c);
-                        if (!(piv > 0.0)) okw = false;
-                        const double inv = rsqrt(piv);          // dpotf2 scales by 1/ajj
-                        const double lcc = piv * inv;
-                        if (r == c) d[c] = lcc;
-                        else if (r > c) d[c] = d[c] * inv;
-#pragma unroll
-                        for (int k = c + 1; k < 8; ++k) {
-                            const double lkc = __shfl_sync(FULL, d[c], k);
-                            if (r >= k) d[k] = fma(-d[c], lkc, d[k]);
-                        }
-                        if (lane == c) INV[j0 + c] = inv;
-                    }
-                    if (lane < 8) {                   // separate buffer: other warps may
-#pragma unroll                                        // still be reading the block in L
-                        for (int k = 0; k < 8; ++k) LDG[(j0 + r) * 8 + k] = (k <= r) ? d[k] : 0.0;
-                    }
-                    if (warp == 0 && lane == 0) smem[lay.FLAG] = okw ? 1.0 : 0.0;
-                    __syncwarp();
-                }
-                // (c) rows below the block: L(i, J) = A(i, J) L_JJ^-T
-                for (int i = j0 + 8 + tid; i < n8; i += NT) {
-                    double v[8];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        double t = L[CO[j0 + c] + i];
-#pragma unroll
-                        for (int k = 0; k < c; ++k) t = fma(-v[k], LDG[(j0 + c) * 8 + k], t);
-                        v[c] = t * INV[j0 + c];
-                    }
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) L[CO[j0 + c] + i] = v[c];
+                    chol_diag_and_rows(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
                 }
                 __syncthreads();
                 la_prev = la;
@@ -2283,16 +2311,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
             ok = true;
             // DMMA update of one 8x8 row tile of panel `jp` with columns [k_lo, k_hi)
             auto tile_update = [&](int t, int jp, int k_lo, int k_hi) {
-                const int rb = t * 8;
-                double c0 = L[CO[jp + 2 * tig] + rb + g];
-                double c1 = L[CO[jp + 2 * tig + 1] + rb + g];
-                for (int k4 = k_lo; k4 < k_hi; k4 += 4) {
-                    const double a = -L[CO[k4 + tig] + rb + g];
-                    const double b = L[CO[k4 + tig] + jp + g];
-                    dmma_acc(c0, c1, a, b);
-                }
-                L[CO[jp + 2 * tig] + rb + g] = c0;
-                L[CO[jp + 2 * tig + 1] + rb + g] = c1;
+                chol_tile_update(L, CO, n8, t, jp, k_lo, k_hi, g, tig);
             };
             bool la_prev = false;   // look-ahead already applied columns < j0 - 8 to this panel
             for (int kb = 0; kb < nrb; ++kb) {
@@ -2304,13 +2323,11 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
                     for (int t = kb + warp; t < nrb; t += NW) tile_update(t, j0, klo, j0);
                     __syncthreads();
                 }
-                // (b) the warps that solve rows below this block (and warp 0, which
-                // publishes INV / LDG / the pivot flag) factor the 8x8 diagonal block
-                // redundantly (lane r holds row r).  Identical inputs give identical
-                // outputs, so the duplicate shared-memory stores are benign and no
-                // barrier separates the factorisation from the rows below.  The other
-                // warps meanwhile apply every final column (< j0) to the NEXT panel
-                // (look-ahead), hiding the serial factorisation behind the GEMM work.
+                // (b) every thread of the warps that own rows below this block (warp 0
+                // at least) factors the 8x8 diagonal block in its own registers and
+                // solves its row against it: no shuffles and no barrier between the
+                // two.  The other warps meanwhile apply every final column (< j0) to
+                // the NEXT panel (look-ahead), hiding the serial factorisation.
                 const int below = n8 - j0 - 8;
                 const int nfw = below > 32 ? (below + 31) / 32 : 1;
                 const bool la = (kb + 1 < nrb) && (NW > nfw) && j0 > 0;
@@ -2319,45 +2336,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
                         for (int t = kb + 1 + (warp - nfw); t < nrb; t += NW - nfw)
                             tile_update(t, j0 + 8, 0, j0);
                 } else {
-                    double d[8];
-                    const int r = lane & 7;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) d[k] = (k <= r) ? L[CO[j0 + k] + j0 + r] : 0.0;
-                    bool okw = true;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const double piv = __shfl_sync(FULL, d[c], c);
-                        if (!(piv > 0.0)) okw = false;
-                        const double inv = rsqrt(piv);          // dpotf2 scales by 1/ajj
-                        const double lcc = piv * inv;
-                        if (r == c) d[c] = lcc;
-                        else if (r > c) d[c] = d[c] * inv;
-#pragma unroll
-                        for (int k = c + 1; k < 8; ++k) {
-                            const double lkc = __shfl_sync(FULL, d[c], k);
-                            if (r >= k) d[k] = fma(-d[c], lkc, d[k]);
-                        }
-                        if (lane == c) INV[j0 + c] = inv;
-                    }
-                    if (lane < 8) {                   // separate buffer: other warps may
-#pragma unroll                                        // still be reading the block in L
-                        for (int k = 0; k < 8; ++k) LDG[(j0 + r) * 8 + k] = (k <= r) ? d[k] : 0.0;
-                    }
-                    if (warp == 0 && lane == 0) smem[lay.FLAG] = okw ? 1.0 : 0.0;
-                    __syncwarp();
-                }
-                // (c) rows below the block: L(i, J) = A(i, J) L_JJ^-T
-                for (int i = j0 + 8 + tid; i < n8; i += NT) {
-                    double v[8];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        double t = L[CO[j0 + c] + i];
-#pragma unroll
-                        for (int k = 0; k < c; ++k) t = fma(-v[k], LDG[(j0 + c) * 8 + k], t);
-                        v[c] = t * INV[j0 + c];
-                    }
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) L[CO[j0 + c] + i] = v[c];
+                    chol_diag_and_rows(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
                 }
                 __syncthreads();
                 la_prev = la;
