@@ -326,12 +326,12 @@ def run_gpu(args, rank, world, local_rank):
     top = max(stages, key=lambda k: stages[k][0])
     top_ms, top_n = stages[top]
     sol = counts[counts >= TAU]
-    bucket = {"gpr_warp16": sol[sol <= 16], "gpr_warp24": sol[(sol > 16) & (sol <= 24)],
-              "gpr_warp32": sol[(sol > 24) & (sol <= 32)],
-              "gpr_tile64": sol[(sol > 32) & (sol <= 64)],
-              "gpr_tile96": sol[(sol > 64) & (sol <= 96)],
-              "gpr_tile128": sol[(sol > 96) & (sol <= 128)],
-              "gpr_cta160": sol[(sol > 128) & (sol <= 160)], "gpr_cta_large": sol[sol > 160]}
+    bucket = {"gpr_n16": sol[sol <= 16], "gpr_n24": sol[(sol > 16) & (sol <= 24)],
+              "gpr_n32": sol[(sol > 24) & (sol <= 32)],
+              "gpr_n64": sol[(sol > 32) & (sol <= 64)],
+              "gpr_n96": sol[(sol > 64) & (sol <= 96)],
+              "gpr_n128": sol[(sol > 96) & (sol <= 128)],
+              "gpr_n160": sol[(sol > 128) & (sol <= 160)], "gpr_n_large": sol[sol > 160]}
     if top in bucket:
         flops = float(gpr_flops(bucket[top]).sum()) * args.steps
         achieved = flops / (top_ms / 1e3) / 1e12

@@ -318,10 +318,10 @@ int vx_pack_map_records(const VxGaussianOut* records, int64_t count, void* d_out
 int vx_fp64_peak(double* tflops, void* stream);
 
 /* CUDA-event timers around the library's stages, recorded on the launching
- * stream: 0 store_frame (hashing), 1-2 GPR warp kernels n<=16/24,
- * 3-4 GPR DMMA tile kernels n<=64/128, 5 GPR CTA kernel n>128, 6 warp kernel
- * n<=32, 7 DMMA tile kernel n<=96, 8 CTA kernel 128<n<=160, 9 Gaussian
- * init, 10 whole densify, 11 PCA prepass.  vx_profile(1) resets
+ * stream: 0 store_frame (hashing); GPR solves by training-set size bucket:
+ * 1 n<=16, 2 n<=24, 6 n<=32 (warp-per-voxel DMMA kernels), 3 n<=64,
+ * 7 n<=96, 4 n<=128 (DMMA tile kernels), 8 n<=160, 5 n>160 (large-n
+ * kernels); 9 Gaussian init, 10 whole densify, 11 PCA prepass.  vx_profile(1) resets
  * and enables; vx_profile_read fills total ms and launch counts per stage
  * and returns the number of stages. */
 int vx_profile(int enable);

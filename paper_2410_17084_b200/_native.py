@@ -261,8 +261,8 @@ def splat_struct(n_s, n_r, weight_floor, scale_floor, opacity, rotation="identit
     return s
 
 
-PROFILE_STAGES = ("hash", "gpr_warp16", "gpr_warp24", "gpr_tile64", "gpr_tile128", "gpr_cta_large",
-                  "gpr_warp32", "gpr_tile96", "gpr_cta160", "splat", "densify", "pca")
+PROFILE_STAGES = ("hash", "gpr_n16", "gpr_n24", "gpr_n64", "gpr_n128", "gpr_n_large",
+                  "gpr_n32", "gpr_n96", "gpr_n160", "splat", "densify", "pca")
 
 
 def profile(enable: bool) -> None:

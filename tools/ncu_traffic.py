@@ -25,14 +25,14 @@ col = {h: i for i, h in enumerate(hdr)}
 _, _, counts, *_ = bench.make_workload(V, 0)
 sol = counts[counts >= bench.TAU]
 # launch order within one densify is bucket id 7, 6, 5, 4, 3, 2, 1, 0 (largest first)
-buckets = [("gpr_cta_kernel", (128, 160), "gpr_cta160"),
-           ("gpr_tile_kernel<16, 1, 12", (64, 96), "gpr_tile96"),
-           ("gpr_warp_kernel<32", (24, 32), "gpr_warp32"),
-           ("gpr_cta_kernel", (160, 10 ** 9), "gpr_cta_large"),
-           ("gpr_tile_kernel<16, 1, 12", (96, 128), "gpr_tile128"),
-           ("gpr_tile_kernel<8", (32, 64), "gpr_tile64"),
-           ("gpr_warp_kernel<24", (16, 24), "gpr_warp24"),
-           ("gpr_warp_kernel<16", (0, 16), "gpr_warp16")]
+buckets = [("gpr_big_kernel<12", (128, 160), "gpr_n160"),
+           ("gpr_tile_kernel<16, 2, 6", (64, 96), "gpr_n96"),
+           ("gpr_wdmma_kernel<32", (24, 32), "gpr_n32"),
+           ("gpr_big_kernel<12", (160, 10 ** 9), "gpr_n_large"),
+           ("gpr_tile_kernel<16, 2, 6", (96, 128), "gpr_n128"),
+           ("gpr_tile_kernel<8, 2, 6", (32, 64), "gpr_n64"),
+           ("gpr_wdmma_kernel<24", (16, 24), "gpr_n24"),
+           ("gpr_wdmma_kernel<16", (0, 16), "gpr_n16")]
 res = {}
 for r in rows[2:]:
     name = r[col["Kernel Name"]]
