@@ -36,11 +36,9 @@ buckets = [("gpr_big_kernel<12", (128, 160), "gpr_n160"),
 res = {}
 for r in rows[2:]:
     name = r[col["Kernel Name"]]
-    rd = float(r[col["dram__bytes_read.sum"]])
-    wr = float(r[col["dram__bytes_write.sum"]])
-    unit = rows[1][col["dram__bytes_read.sum"]]
-    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-    tot = (rd + wr) * mult
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = sum(float(r[col[m]]) * scale.get(rows[1][col[m]], 1)     # per-column units
+              for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     for key, (lo, hi), label in buckets:
         if key in name and label not in res:
             n = int(((sol > lo) & (sol <= hi)).sum())
