@@ -1635,6 +1635,39 @@ struct TileLayout {
     }
 };
 
+// A = K + diag(noise) (+ jitter on the retry), identity-padded to n8 rows,
+// into the packed lower triangle (gpr.py:184-186).  Thread = lower-triangle
+// entry (single-precision root + fix-up decode); two entries per iteration
+// with branch-free selects so their exp chains interleave.
+__device__ __forceinline__ void team_fill_matrix(double* L, const int* CO, const double* X,
+                                                 const double* NZ, int n, int n8, int kind,
+                                                 double lam, double jit, int tid, int nt) {
+    const int tot = n8 * (n8 + 1) / 2;
+    for (int e0 = tid; e0 < tot; e0 += 2 * nt) {
+        double v[2];
+        int dst[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = e0 + u * nt;
+            int i = int((sqrtf(8.0f * float(e) + 1.0f) - 1.0f) * 0.5f);
+            if ((i + 1) * (i + 2) / 2 <= e) ++i;
+            if (i * (i + 1) / 2 > e) --i;
+            const int j = e - i * (i + 1) / 2;
+            const int ic = i < n8 ? i : n8 - 1;       // e >= tot: discarded below
+            const int jc = j < n8 ? j : 0;
+            const double kv = kernel_value(kind, lam, dist2_exact(X[2 * ic], X[2 * ic + 1],
+                                                                  X[2 * jc], X[2 * jc + 1]));
+            double dg = xadd(1.0, NZ[ic]);
+            if (jit != 0.0) dg = xadd(dg, jit);
+            v[u] = i >= n ? (i == j ? 1.0 : 0.0) : (i == j ? dg : kv);
+            dst[u] = e < tot ? CO[jc] + ic : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (dst[u] >= 0) L[dst[u]] = v[u];
+    }
+}
+
 // Cholesky update of the 8x8 tile (rows 8t.., panel columns jp..jp+7):
 // A -= L(rows, k_lo:k_hi) L(panel, k_lo:k_hi)^T with DMMA; k_lo, k_hi are
 // multiples of 8 and the two k-chunks of each block column feed separate
@@ -1775,6 +1808,7 @@ __device__ __forceinline__ void team_se_tables(double* EA, double* EB, const dou
         const double xi = X[2 * i + which];
         const double* G = GC + which * mm;
         double* T = (which ? EB : EA) + i * mm;
+#pragma unroll 3
         for (int r = 0; r < mm; ++r) {
             const double d = xsub(xi, G[r]);
             T[r] = exp(xmul(-lam, xmul(d, d)));
@@ -1953,24 +1987,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
         bool ok = false;
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? jitter : 0.0;
-            const int tot = n8 * (n8 + 1) / 2;
-            for (int e = tid; e < tot; e += NT) {
-                // lower-triangle index -> (i, j): single-precision root + one fix-up
-                int i = int((sqrtf(8.0f * float(e) + 1.0f) - 1.0f) * 0.5f);
-                if ((i + 1) * (i + 2) / 2 <= e) ++i;
-                if (i * (i + 1) / 2 > e) --i;
-                const int j = e - i * (i + 1) / 2;
-                double v;
-                if (i >= n) {
-                    v = (i == j) ? 1.0 : 0.0;
-                } else if (i == j) {
-                    v = xadd(1.0, NZ[i]);
-                    if (jit != 0.0) v = xadd(v, jit);
-                } else {
-                    v = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
-                }
-                L[CO[j] + i] = v;
-            }
+            team_fill_matrix(L, CO, X, NZ, n, n8, kind, lam, jit, tid, NT);
             __syncthreads();
             ok = true;
             // DMMA update of one 8x8 row tile of panel `jp` with columns [k_lo, k_hi)
@@ -2289,24 +2306,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
         bool ok = false;
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? jitter : 0.0;
-            const int tot = n8 * (n8 + 1) / 2;
-            for (int e = tid; e < tot; e += NT) {
-                // lower-triangle index -> (i, j): single-precision root + one fix-up
-                int i = int((sqrtf(8.0f * float(e) + 1.0f) - 1.0f) * 0.5f);
-                if ((i + 1) * (i + 2) / 2 <= e) ++i;
-                if (i * (i + 1) / 2 > e) --i;
-                const int j = e - i * (i + 1) / 2;
-                double v;
-                if (i >= n) {
-                    v = (i == j) ? 1.0 : 0.0;
-                } else if (i == j) {
-                    v = xadd(1.0, NZ[i]);
-                    if (jit != 0.0) v = xadd(v, jit);
-                } else {
-                    v = kernel_value(kind, lam, dist2_exact(X[2 * i], X[2 * i + 1], X[2 * j], X[2 * j + 1]));
-                }
-                L[CO[j] + i] = v;
-            }
+            team_fill_matrix(L, CO, X, NZ, n, n8, kind, lam, jit, tid, NT);
             __syncthreads();
             ok = true;
             // DMMA update of one 8x8 row tile of panel `jp` with columns [k_lo, k_hi)
