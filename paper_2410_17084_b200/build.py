@@ -25,6 +25,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
+# diagnostics builds only, e.g. VX_EXTRA_NVCC_FLAGS=-DVX_PHASE_TIMING (tools/phase_timing.py)
+FLAGS += os.environ.get("VX_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _sources():

@@ -30,12 +30,31 @@
 // voxel's prediction slot — which is also the pseudo-observation set of its
 // next solve — and update the lifecycle state in the same kernel.
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "vx_common.cuh"
 #include "vx_internal.h"
 
 namespace vx {
+
+// Diagnostics build (-DVX_PHASE_TIMING): thread 0 of every tile-kernel CTA
+// adds the SM clock cycles of each phase of each voxel to g_phase_cycles,
+// read back (and reset) by the extra export vx_phase_cycles
+// (tools/phase_timing.py).  Compiled out otherwise.
+#ifdef VX_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[8];
+#define VX_PHASE(id, t0)                                                                  \
+    do {                                                                                  \
+        if (threadIdx.x == 0) {                                                           \
+            const long long t1_ = clock64();                                              \
+            atomicAdd(&g_phase_cycles[id], (unsigned long long)(t1_ - (t0)));             \
+            (t0) = t1_;                                                                   \
+        }                                                                                 \
+    } while (0)
+#else
+#define VX_PHASE(id, t0) do { } while (0)
+#endif
 
 constexpr int MAX_MM = 16;   // n_s * n_r <= 16 (grid 4..16 per axis sweep)
 
@@ -1931,6 +1950,9 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
     }
 
     for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
+#ifdef VX_PHASE_TIMING
+        long long tph = clock64();
+#endif
         int n, m, s, vid = 0, cnt = 0, slot = 0, axis = 2;
         int64_t off = 0, xo = 0, qo = 0;
         double lam, jitter, mean_f = 0.0;
@@ -1982,6 +2004,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
             CO[j] = o + (j & 7) * tile_ldb(n8, kb) - 8 * kb;
         }
         __syncthreads();
+        VX_PHASE(0, tph);                     // staging, grid, SE tables
 
         // ---- A (identity-padded), panel Cholesky with DMMA updates, one retry
         bool ok = false;
@@ -1989,6 +2012,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
             const double jit = attempt ? jitter : 0.0;
             team_fill_matrix(L, CO, X, NZ, n, n8, kind, lam, jit, tid, NT);
             __syncthreads();
+            VX_PHASE(1, tph);                 // kernel matrix
             ok = true;
             // DMMA update of one 8x8 row tile of panel `jp` with columns [k_lo, k_hi)
             auto tile_update = [&](int t, int jp, int k_lo, int k_hi) {
@@ -2028,6 +2052,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
             }
             __syncthreads();
         }
+        VX_PHASE(2, tph);                     // panel Cholesky
         if (!ok) {
             if (tid == 0) {
                 if constexpr (VOXEL) {
@@ -2066,6 +2091,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
         }
         __syncthreads();
 
+        VX_PHASE(3, tph);                     // diagonal-block inverses
         // ---- forward substitution: right-hand sides resident as DMMA accumulators
         const int ncols = m + 1;
         const double* EA = smem + lay.EA;
@@ -2204,6 +2230,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
             if constexpr (VOXEL) {
                 // voxel mode: m + 1 <= PCOLS (asserted by the launcher), one pass
                 __syncthreads();
+                VX_PHASE(4, tph);             // forward substitution + reductions
                 team_voxel_epilogue(va, vc, X, GC, QT, mm, smem + lay.MU, smem + lay.VAR,
                                     smem + lay.COL, tid, NT);
             }
@@ -2213,6 +2240,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
             if (tid == 0) pa.status[s] = VX_ST_OK;
         }
         __syncthreads();
+        VX_PHASE(5, tph);                     // epilogue
     }
 }
 
@@ -2517,6 +2545,9 @@ static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     int per_sm = int((size_t(227) * 1024) / (smem + 1024));
     if (per_sm < 1) per_sm = 1;
     if (per_sm > 8) per_sm = 8;
+#ifdef VX_PHASE_TIMING
+    if (getenv("VX_TILE_PER_SM")) per_sm = atoi(getenv("VX_TILE_PER_SM"));
+#endif
     int blocks = num_items;
     const int cap = sm_count() * per_sm;
     if (blocks > cap) blocks = cap;
@@ -2726,3 +2757,16 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
 }
 
 }  // namespace vx
+
+#ifdef VX_PHASE_TIMING
+// diagnostics-build export: copy out and reset the per-phase cycle sums
+extern "C" int vx_phase_cycles(unsigned long long* out, int max_phases) {
+    unsigned long long h[8];
+    if (cudaMemcpyFromSymbol(h, vx::g_phase_cycles, sizeof(h)) != cudaSuccess) return -1;
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(vx::g_phase_cycles, z, sizeof(z));
+    const int k = max_phases < 8 ? max_phases : 8;
+    for (int i = 0; i < k; ++i) out[i] = h[i];
+    return k;
+}
+#endif

@@ -1,0 +1,80 @@
+// FP64 tensor-core (m8n8k4 DMMA) and DFMA throughput microbenchmark (B200).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/dmma_peak.cu -o /tmp/dmma_peak && /tmp/dmma_peak
+#include <cstdio>
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+template <int CH>
+__global__ void k_dmma(double* out, int iters) {
+    double c[CH][2];
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) c[i][0] = c[i][1] = 0.0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < CH; ++i) dmma(c[i][0], c[i][1], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) s += c[i][0] + c[i][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <int CH>
+__global__ void k_dfma(double* out, int iters) {
+    double c[CH];
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) c[i] = i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < CH; ++i) c[i] = fma(a, c[i], b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) s += c[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <typename K>
+float time_it(K kern, int blocks, int threads, double* out, int iters) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    kern<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e0);
+    kern<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms;
+}
+
+int main() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    double* out;
+    cudaMalloc(&out, size_t(sms) * 64 * 1024 * 8);
+    const int iters = 4096;
+    for (int wps : {1, 2, 4, 8, 16}) {
+        const int blocks = sms, threads = 32 * wps;
+        float ms = time_it(k_dmma<8>, blocks, threads, out, iters);
+        double flops = double(blocks) * wps * iters * 8 * 512.0;   // 8x8x4 x2 flops per mma
+        printf("DMMA  %2d warps/SM x 8 chains: %7.2f TFLOP/s  (%.2f cycles/mma/SM at 1.965 GHz)\n", wps,
+               flops / ms / 1e9, (ms * 1e-3 * 1.965e9) / (double(wps) * iters * 8));
+        ms = time_it(k_dmma<1>, blocks, threads, out, iters);
+        flops = double(blocks) * wps * iters * 1 * 512.0;
+        printf("DMMA  %2d warps/SM x 1 chain : %7.2f TFLOP/s  (latency %.1f cycles if 1 warp)\n", wps,
+               flops / ms / 1e9, (ms * 1e-3 * 1.965e9) / iters);
+    }
+    for (int wps : {4, 8, 16, 32}) {
+        float ms = time_it(k_dfma<8>, sms, 32 * wps, out, iters);
+        double flops = double(sms) * 32 * wps * iters * 8 * 2.0;
+        printf("DFMA  %2d warps/SM x 8 chains: %7.2f TFLOP/s\n", wps, flops / ms / 1e9);
+    }
+    return 0;
+}
