@@ -78,3 +78,57 @@ int main() {
     }
     return 0;
 }
+
+// dependent-chain latencies (one warp), cycles per operation
+__global__ void k_lat(double* out, long long* cyc, int iters) {
+    double x = 1.0 + threadIdx.x * 1e-12, y = 0.999999;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) x = fma(x, y, 1e-9);
+    long long t1 = clock64();
+    for (int i = 0; i < iters; ++i) x = rsqrt(x) + 0.5;
+    long long t2 = clock64();
+    for (int i = 0; i < iters; ++i) x = __dmul_rn(x, y);
+    long long t3 = clock64();
+    out[threadIdx.x] = x;
+    if (threadIdx.x == 0) {
+        cyc[0] = (t1 - t0) / iters;
+        cyc[1] = (t2 - t1) / iters;
+        cyc[2] = (t3 - t2) / iters;
+    }
+}
+
+__global__ void k_shfl_lat(double* out, long long* cyc, int iters) {
+    double x = threadIdx.x;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) x = __shfl_sync(0xffffffffu, x, (threadIdx.x + 1) & 31) + 1.0;
+    long long t1 = clock64();
+    out[threadIdx.x] = x;
+    if (threadIdx.x == 0) cyc[3] = (t1 - t0) / iters;
+}
+
+__global__ void k_lds_lat(double* out, long long* cyc, int iters) {
+    __shared__ int buf[1024];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) buf[i] = (i + 1) & 1023;
+    __syncthreads();
+    int p = threadIdx.x;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) p = buf[p];
+    long long t1 = clock64();
+    out[threadIdx.x] = p;
+    if (threadIdx.x == 0) cyc[4] = (t1 - t0) / iters;
+}
+
+int lat_main() {
+    double* out;
+    long long* cyc;
+    cudaMalloc(&out, 4096);
+    cudaMallocManaged(&cyc, 64);
+    k_lat<<<1, 32>>>(out, cyc, 4096);
+    k_shfl_lat<<<1, 32>>>(out, cyc, 4096);
+    k_lds_lat<<<1, 32>>>(out, cyc, 4096);
+    cudaDeviceSynchronize();
+    printf("latency (cycles): DFMA %lld, rsqrt(double)+add %lld, DMUL %lld, SHFL+DADD %lld, LDS.32 %lld\n",
+           cyc[0], cyc[1], cyc[2], cyc[3], cyc[4]);
+    return 0;
+}
+static int dummy = lat_main();

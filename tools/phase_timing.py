@@ -22,29 +22,29 @@ import paper_2410_17084_b200 as vx  # noqa: E402
 from paper_2410_17084_b200 import _native as N  # noqa: E402
 from workloads import scenes  # noqa: E402
 
-PHASES = ("stage", "fill", "chol", "linv", "trsm", "epilogue")
+PHASES = ("stage", "fill", "chol", "linv", "trsm", "epilogue", "chol.update", "chol.factor", "chol.barrier")
 
 
 def main():
     lib = N.lib()
     fn = lib.vx_phase_cycles
     fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-    buf = (ctypes.c_ulonglong * 8)()
+    buf = (ctypes.c_ulonglong * 12)()
     for lo, hi in ((33, 64), (65, 96), (97, 128)):
         pos, col, counts, keys, owner = scenes.planar_map(20000, voxel_size=0.5, seed=1,
                                                           bins=[(lo, hi + 1)], probs=[1.0])
         eng = vx.MappingEngine(vx.PipelineConfig(voxel_size=0.5))
         eng.ingest(pos, col)                     # warm-up (and JIT of nothing)
         eng = vx.MappingEngine(vx.PipelineConfig(voxel_size=0.5))
-        fn(buf, 8)
+        fn(buf, 12)
         rep = eng.ingest(pos, col)
         import torch
         torch.cuda.synchronize()
-        fn(buf, 8)
+        fn(buf, 12)
         solved = max(int(getattr(rep, "voxels_solved", len(counts))), 1)
-        cyc = np.array(buf[:6], dtype=np.float64) / solved
+        cyc = np.array(buf[:9], dtype=np.float64) / solved
         print(f"n {lo:3d}-{hi:3d} voxels {solved:6d} " +
-              " ".join(f"{p}={c:8.0f}" for p, c in zip(PHASES, cyc)) + f" total={cyc.sum():8.0f}")
+              " ".join(f"{p}={c:8.0f}" for p, c in zip(PHASES, cyc)) + f" total={cyc[:6].sum():8.0f}")
 
 
 if __name__ == "__main__":
