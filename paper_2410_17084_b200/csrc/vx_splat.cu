@@ -20,6 +20,7 @@
 namespace vx {
 
 constexpr double SH0_BASIS = 0.28209479177;   // splat_init.py:22
+constexpr int MAX_SUB = 256;                   // n_r^2 with n_s * n_r <= 16
 
 struct SplatArgs {
     const double* pxyz;
@@ -109,14 +110,17 @@ int launch_init_color(const double* pos, const double* fallback, int64_t n, cons
     return VX_OK;
 }
 
-template <bool EIGEN>
+template <bool EIGEN, int KT>
 __global__ void __launch_bounds__(256) gaussians_kernel(SplatArgs a) {
+    // KT = n_r^2 points per subgrid for the common grids (weights in registers);
+    // KT = 0: any n_r <= 16 with a runtime loop (weights in local memory)
+    constexpr int KW = KT > 0 ? KT : MAX_SUB;
+    const int K = KT > 0 ? KT : a.n_r * a.n_r;
     const int nsub = a.n_s * a.n_s;
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (gid >= a.count * nsub) return;
     const int64_t v = gid / nsub;
     const int b = int(gid - v * nsub);
-    const int k = a.n_r * a.n_r;
     int64_t base;
     const int64_t* key;
     if (a.voxel_ids) {
@@ -127,23 +131,26 @@ __global__ void __launch_bounds__(256) gaussians_kernel(SplatArgs a) {
         base = v * a.M;
         key = a.dkeys + v * 3;
     }
-    base += int64_t(b) * k;
+    base += int64_t(b) * K;
     const double* P = a.pxyz + base * 3;
     const double* C = a.prgb + base * 3;
     const double* S = a.pvar + base;
     const double wf = a.cfg.weight_floor;
-    auto weight = [&](int i) { return xdiv(1.0, fmax(S[i], wf)); };
-    // np.maximum propagates NaN; variances are finite and clipped here
-    const double wsum = np_pairwise_sum(weight, k);
+    // w = 1 / max(sigma^2, floor) once per point (splat_init.py:86); np.maximum
+    // propagates NaN, variances are finite and clipped here
+    double w[KW];
+#pragma unroll
+    for (int i = 0; i < K; ++i) w[i] = xdiv(1.0, fmax(__ldg(S + i), wf));
+    const double wsum = np_pairwise_sum([&](int i) { return w[i]; }, K);
     double px = 0, py = 0, pz = 0, cr = 0, cg = 0, cb = 0;
-    for (int i = 0; i < k; ++i) {
-        const double w = weight(i);
-        px = xadd(px, xmul(P[i * 3 + 0], w));
-        py = xadd(py, xmul(P[i * 3 + 1], w));
-        pz = xadd(pz, xmul(P[i * 3 + 2], w));
-        cr = xadd(cr, xmul(C[i * 3 + 0], w));
-        cg = xadd(cg, xmul(C[i * 3 + 1], w));
-        cb = xadd(cb, xmul(C[i * 3 + 2], w));
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        px = xadd(px, xmul(__ldg(P + i * 3 + 0), w[i]));
+        py = xadd(py, xmul(__ldg(P + i * 3 + 1), w[i]));
+        pz = xadd(pz, xmul(__ldg(P + i * 3 + 2), w[i]));
+        cr = xadd(cr, xmul(__ldg(C + i * 3 + 0), w[i]));
+        cg = xadd(cg, xmul(__ldg(C + i * 3 + 1), w[i]));
+        cb = xadd(cb, xmul(__ldg(C + i * 3 + 2), w[i]));
     }
     px = xdiv(px, wsum);
     py = xdiv(py, wsum);
@@ -152,11 +159,11 @@ __global__ void __launch_bounds__(256) gaussians_kernel(SplatArgs a) {
     cg = xdiv(cg, wsum);
     cb = xdiv(cb, wsum);
     double phi[6] = {0, 0, 0, 0, 0, 0};   // xx xy xz yy yz zz
-    for (int i = 0; i < k; ++i) {
-        const double w = weight(i);
-        const double qx = xsub(P[i * 3 + 0], px), qy = xsub(P[i * 3 + 1], py),
-                     qz = xsub(P[i * 3 + 2], pz);
-        const double wx = qx * w, wy = qy * w, wz = qz * w;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const double qx = xsub(__ldg(P + i * 3 + 0), px), qy = xsub(__ldg(P + i * 3 + 1), py),
+                     qz = xsub(__ldg(P + i * 3 + 2), pz);
+        const double wx = qx * w[i], wy = qy * w[i], wz = qz * w[i];
         phi[0] = fma(wx, qx, phi[0]);
         phi[1] = fma(wx, qy, phi[1]);
         phi[2] = fma(wx, qz, phi[2]);
@@ -209,10 +216,18 @@ int launch_gaussians(const double* pred_xyz, const double* pred_rgb, const doubl
     SplatArgs a{pred_xyz, pred_rgb, pred_var, slot_of, voxel_ids, keys, direct_keys, count,
                 M, cfg.n_s, cfg.n_r, cam, image, cfg, out};
     const int64_t threads = count * cfg.n_s * cfg.n_s;
-    if (cfg.rotation_mode == VX_ROT_EIGEN)
-        gaussians_kernel<true><<<unsigned((threads + 255) / 256), 256, 0, s>>>(a);
-    else
-        gaussians_kernel<false><<<unsigned((threads + 255) / 256), 256, 0, s>>>(a);
+    const unsigned blocks = unsigned((threads + 255) / 256);
+    const bool eig = cfg.rotation_mode == VX_ROT_EIGEN;
+    switch (cfg.n_r) {
+        case 2: eig ? gaussians_kernel<true, 4><<<blocks, 256, 0, s>>>(a)
+                    : gaussians_kernel<false, 4><<<blocks, 256, 0, s>>>(a); break;
+        case 3: eig ? gaussians_kernel<true, 9><<<blocks, 256, 0, s>>>(a)
+                    : gaussians_kernel<false, 9><<<blocks, 256, 0, s>>>(a); break;
+        case 4: eig ? gaussians_kernel<true, 16><<<blocks, 256, 0, s>>>(a)
+                    : gaussians_kernel<false, 16><<<blocks, 256, 0, s>>>(a); break;
+        default: eig ? gaussians_kernel<true, 0><<<blocks, 256, 0, s>>>(a)
+                     : gaussians_kernel<false, 0><<<blocks, 256, 0, s>>>(a); break;
+    }
     count_launch();
     VX_CHECK_LAUNCH();
     return VX_OK;
