@@ -1930,7 +1930,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
     constexpr int N8 = NRB * 8;
     constexpr int NT = NW * 32;
     constexpr int PCOLS = NW * CTW * 8;             // right-hand sides per pass
-    const TileLayout lay(N8, mm, PCOLS, mmax, VOXEL);
+    const int MC = mmax + 1 > PCOLS ? mmax + 1 : PCOLS;   // columns of [f | K*] (padded)
+    const TileLayout lay(N8, mm, MC, mmax, VOXEL);
     double* L = smem + lay.L;
     double* X = smem + lay.X;
     double* F = smem + lay.F;
@@ -1945,7 +1946,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
     double* GC = smem + lay.GC;
     int* QT = reinterpret_cast<int*>(smem + lay.QT);
     if constexpr (VOXEL) {
-        team_query_table(QT, va, PCOLS, tid, NT);
+        team_query_table(QT, va, MC, tid, NT);
         __syncthreads();
     }
 
@@ -2218,8 +2219,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
                     if (g == 0 && c > 0 && c < ncols) {
                         const double var = 1.0 - ss;
                         if constexpr (VOXEL) {
-                            smem[lay.MU + lc] = xadd(mu, mean_f);
-                            smem[lay.VAR + lc] = var < 0.0 ? 0.0 : var;
+                            smem[lay.MU + c] = xadd(mu, mean_f);      // by global column
+                            smem[lay.VAR + c] = var < 0.0 ? 0.0 : var;
                         } else {
                             pa.mu[qo + c - 1] = mu;
                             pa.var[qo + c - 1] = var;
@@ -2227,14 +2228,13 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
                     }
                 }
             }
-            if constexpr (VOXEL) {
-                // voxel mode: m + 1 <= PCOLS (asserted by the launcher), one pass
-                __syncthreads();
-                VX_PHASE(4, tph);             // forward substitution + reductions
-                team_voxel_epilogue(va, vc, X, GC, QT, mm, smem + lay.MU, smem + lay.VAR,
-                                    smem + lay.COL, tid, NT);
-            }
             __syncthreads();
+        }
+        if constexpr (VOXEL) {
+            // every pass has written MU / VAR (indexed by column): epilogue once
+            VX_PHASE(4, tph);                 // forward substitution + reductions
+            team_voxel_epilogue(va, vc, X, GC, QT, mm, smem + lay.MU, smem + lay.VAR,
+                                smem + lay.COL, tid, NT);
         }
         if constexpr (!VOXEL) {
             if (tid == 0) pa.status[s] = VX_ST_OK;
@@ -2534,11 +2534,8 @@ static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
                        int mm, cudaStream_t s) {
     if (num_items <= 0) return VX_OK;
     constexpr int PCOLS = NW * CTW * 8;
-    if (VOXEL && m_max + 1 > PCOLS) {
-        set_error("tile kernel: %d right-hand sides exceed %d", m_max + 1, PCOLS);
-        return VX_E_INPUT;
-    }
-    const TileLayout lay(NRB * 8, mm, PCOLS, m_max, VOXEL);
+    const int MC = m_max + 1 > PCOLS ? m_max + 1 : PCOLS;
+    const TileLayout lay(NRB * 8, mm, MC, m_max, VOXEL);
     const size_t smem = size_t(lay.total) * sizeof(double);
     auto kfn = gpr_tile_kernel<NRB, CTW, NW, VOXEL>;
     VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -2717,19 +2714,16 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 0: return launch_wdmma<16>(a, mm, s);
         case 1: return launch_wdmma<24>(a, mm, s);
         case 5: return launch_wdmma<32>(a, mm, s);
-        case 2:   // 32 < n <= 64: two 6-warp CTAs per SM, right-hand sides in registers
-            if (a.M + 1 <= 96) return launch_tile<8, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
-            return launch_big<6, true>(a, none, a.num_items, max_n < 64 ? max_n : 64, a.M, mm, work, s);
-        case 6:   // 64 < n <= 96: same kernel as n <= 128 (rows beyond n skipped)
-            if (a.M + 1 <= 96) return launch_tile<16, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
-            return launch_big<6, true>(a, none, a.num_items, max_n < 96 ? max_n : 96, a.M, mm, work, s);
+        case 2:   // 32 < n <= 64: two 6-warp CTAs per SM, 2 x 8 right-hand sides per warp
+            return launch_tile<8, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
+        case 6:   // 64 < n <= 96: the n <= 128 kernel (rows beyond n skipped)
+            return launch_tile<16, 1, 6, true>(a, none, a.num_items, a.M, mm, s);
+        case 3:   // 96 < n <= 128: two CTAs per SM, one 8-column tile per warp per pass
+            return launch_tile<16, 1, 6, true>(a, none, a.num_items, a.M, mm, s);
         case 7:   // 128 < n <= 160
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n < 160 ? max_n : 160,
                                                            a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 160 ? max_n : 160, a.M, mm, work, s);
-        case 3:   // 96 < n <= 128: register-resident DMMA tile kernel
-            if (a.M + 1 <= 96) return launch_tile<16, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
-            return launch_big<12, true>(a, none, a.num_items, max_n < 128 ? max_n : 128, a.M, mm, work, s);
         default:
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n, a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
@@ -2748,8 +2742,8 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
         if (bucket == 1) return launch_warp<24, false>(none, pa, count, max_m, 1, s);
         if (bucket == 5) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
         if (bucket == 2) return launch_tile<8, 2, 6, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 6) return launch_tile<16, 2, 6, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 3) return launch_tile<16, 2, 6, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 6) return launch_tile<16, 1, 6, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 3) return launch_tile<16, 1, 6, false>(none, pa, count, max_m, 1, s);
 
         return launch_big<12, false>(none, pa, count, max_n, max_m, 1, work, s);
     }
