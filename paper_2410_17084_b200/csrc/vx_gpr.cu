@@ -43,7 +43,7 @@ namespace vx {
 // read back (and reset) by the extra export vx_phase_cycles
 // (tools/phase_timing.py).  Compiled out otherwise.
 #ifdef VX_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[12];
 #define VX_PHASE(id, t0)                                                                  \
     do {                                                                                  \
         if (threadIdx.x == 0) {                                                           \
@@ -1718,11 +1718,21 @@ __device__ __forceinline__ void chol_tile_update(double* L, const int* CO, int n
 __device__ __forceinline__ void chol_diag_and_rows(double* L, const int* CO, double* LDG,
                                                    double* INV, double* flag, int j0, int n8,
                                                    int tid, int nft) {
+#ifdef VX_PHASE_TIMING
+    long long tp = clock64();
+#endif
+    // block column j0/8 is column-major with leading dimension ldb from CO[j0]
+    const int ldb = tile_ldb(n8, j0 >> 3);
+    double* blk = L + CO[j0] + j0;                  // L(j0 + r, j0 + c) = blk[c * ldb + r]
     double a[36];                                   // packed lower triangle, row-major
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c <= r; ++c) a[r * (r + 1) / 2 + c] = L[CO[j0 + c] + j0 + r];
+        for (int c = 0; c <= r; ++c) a[r * (r + 1) / 2 + c] = blk[c * ldb + r];
+#ifdef VX_PHASE_TIMING
+    if (tid == 0) { const double s0 = a[35]; asm volatile("" :: "d"(s0)); }
+#endif
+    VX_PHASE(6, tp);                                // loads
     double inv[8];
     bool ok = true;
 #pragma unroll
@@ -1740,19 +1750,30 @@ __device__ __forceinline__ void chol_diag_and_rows(double* L, const int* CO, dou
                 a[r * (r + 1) / 2 + k] = fma(-a[r * (r + 1) / 2 + c], a[k * (k + 1) / 2 + c],
                                              a[r * (r + 1) / 2 + k]);
     }
-    if (tid == 0) {
+#ifdef VX_PHASE_TIMING
+    if (tid == 0) { const double s1 = a[35] + inv[7]; asm volatile("" :: "d"(s1)); }
+#endif
+    VX_PHASE(7, tp);                                // factorisation chain
+    if (tid < 8) {                                  // thread r publishes row r (selects, no local array)
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int k = 0; k < 8; ++k) {
+            double v = 0.0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) LDG[(j0 + r) * 8 + k] = k <= r ? a[r * (r + 1) / 2 + k] : 0.0;
+            for (int rr = k; rr < 8; ++rr) v = tid == rr ? a[rr * (rr + 1) / 2 + k] : v;
+            LDG[(j0 + tid) * 8 + k] = v;
+        }
+        double iv = inv[0];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) INV[j0 + c] = inv[c];
-        *flag = ok ? 1.0 : 0.0;
+        for (int c = 1; c < 8; ++c) iv = tid == c ? inv[c] : iv;
+        INV[j0 + tid] = iv;
+        if (tid == 0) *flag = ok ? 1.0 : 0.0;
     }
+    VX_PHASE(8, tp);                                // publish
     for (int i = j0 + 8 + tid; i < n8; i += nft) {
         double v[8];
+        double* row = blk + (i - j0);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = L[CO[j0 + c] + i];
+        for (int c = 0; c < 8; ++c) v[c] = row[c * ldb];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             v[c] *= inv[c];
@@ -1760,8 +1781,9 @@ __device__ __forceinline__ void chol_diag_and_rows(double* L, const int* CO, dou
             for (int k = c + 1; k < 8; ++k) v[k] = fma(-v[c], a[k * (k + 1) / 2 + c], v[k]);
         }
 #pragma unroll
-        for (int c = 0; c < 8; ++c) L[CO[j0 + c] + i] = v[c];
+        for (int c = 0; c < 8; ++c) row[c * ldb] = v[c];
     }
+    VX_PHASE(9, tp);                                // rows below
 }
 
 // ---------------------------------------------------------------------------
@@ -2020,6 +2042,9 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
                 chol_tile_update(L, CO, n8, t, jp, k_lo, k_hi, g, tig);
             };
             bool la_prev = false;   // look-ahead already applied columns < j0 - 8 to this panel
+#ifdef VX_PHASE_TIMING
+            long long tsub = clock64();
+#endif
             for (int kb = 0; kb < nrb; ++kb) {
                 const int j0 = kb * 8;
                 // (a) finish the panel update A(i, J) -= L(i, <j0) L(J, <j0)^T: after a
@@ -2029,6 +2054,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
                     for (int t = kb + warp; t < nrb; t += NW) tile_update(t, j0, klo, j0);
                     __syncthreads();
                 }
+                VX_PHASE(10, tsub);               // panel update + barrier
                 // (b) every thread of the warps that own rows below this block (warp 0
                 // at least) factors the 8x8 diagonal block in its own registers and
                 // solves its row against it: no shuffles and no barrier between the
@@ -2044,7 +2070,11 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(Voxe
                 } else {
                     chol_diag_and_rows(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
                 }
+#ifdef VX_PHASE_TIMING
+                tsub = clock64();
+#endif
                 __syncthreads();
+                VX_PHASE(11, tsub);               // barrier after the factorisation
                 la_prev = la;
                 if (smem[lay.FLAG] == 0.0) {          // pivot <= 0 or NaN: uniform exit
                     ok = false;
@@ -2755,11 +2785,11 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
 #ifdef VX_PHASE_TIMING
 // diagnostics-build export: copy out and reset the per-phase cycle sums
 extern "C" int vx_phase_cycles(unsigned long long* out, int max_phases) {
-    unsigned long long h[8];
+    unsigned long long h[12];
     if (cudaMemcpyFromSymbol(h, vx::g_phase_cycles, sizeof(h)) != cudaSuccess) return -1;
-    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long z[12] = {};
     cudaMemcpyToSymbol(vx::g_phase_cycles, z, sizeof(z));
-    const int k = max_phases < 8 ? max_phases : 8;
+    const int k = max_phases < 12 ? max_phases : 12;
     for (int i = 0; i < k; ++i) out[i] = h[i];
     return k;
 }

@@ -22,7 +22,8 @@ import paper_2410_17084_b200 as vx  # noqa: E402
 from paper_2410_17084_b200 import _native as N  # noqa: E402
 from workloads import scenes  # noqa: E402
 
-PHASES = ("stage", "fill", "chol", "linv", "trsm", "epilogue", "chol.update", "chol.factor", "chol.barrier")
+PHASES = ("stage", "fill", "chol", "linv", "trsm", "epilogue", "f.loads", "f.chain", "f.publish",
+          "f.rows", "c.update", "c.barrier")
 
 
 def main():
@@ -42,7 +43,7 @@ def main():
         torch.cuda.synchronize()
         fn(buf, 12)
         solved = max(int(getattr(rep, "voxels_solved", len(counts))), 1)
-        cyc = np.array(buf[:9], dtype=np.float64) / solved
+        cyc = np.array(buf[:12], dtype=np.float64) / solved
         print(f"n {lo:3d}-{hi:3d} voxels {solved:6d} " +
               " ".join(f"{p}={c:8.0f}" for p, c in zip(PHASES, cyc)) + f" total={cyc[:6].sum():8.0f}")
 
