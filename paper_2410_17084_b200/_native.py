@@ -17,7 +17,8 @@ import numpy as np
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libvoxgpr.so")
+# VX_LIB_PATH selects another in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("VX_LIB_PATH") or os.path.join(_HERE, "_lib", "libvoxgpr.so")
 
 VX_OK, VX_E_INPUT, VX_E_CONTRACT, VX_E_CUDA, VX_E_NOMEM, VX_E_RANGE = 0, -1, -2, -3, -4, -5
 ST_OK, ST_DEGENERATE, ST_CHOL_FAIL = 0, 1, 2

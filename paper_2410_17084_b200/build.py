@@ -45,11 +45,13 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Build the library; `out` writes an experiment variant elsewhere (VX_LIB_PATH loads it)."""
+    if out is None and not force and up_to_date():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    lib = out or LIB
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    objdir = os.path.join(os.path.dirname(lib), "obj" if out is None else os.path.basename(lib) + ".obj")
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
@@ -64,14 +66,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    out = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")), None)
+    print(build(force="--force" in sys.argv, verbose=True, out=out))

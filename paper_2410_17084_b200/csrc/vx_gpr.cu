@@ -1945,8 +1945,8 @@ __device__ void team_voxel_epilogue(const VoxelSolveArgs& va, const VoxelCtx& c,
     }
 }
 
-template <int NRB, int CTW, int NW, bool VOXEL>
-__global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
+template <int NRB, int CTW, int NW, int MINB, bool VOXEL>
+__global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
                                                            int mmax, int mm) {
     extern __shared__ __align__(16) double smem[];
     constexpr int N8 = NRB * 8;
@@ -2559,7 +2559,29 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
     }
 }
 
-template <int NRB, int CTW, int NW, bool VOXEL>
+// tile-kernel configurations per size bucket: (8-column tiles per warp and
+// pass, warps per CTA, resident CTAs per SM the registers are capped for)
+#ifndef T64_CTW
+#define T64_CTW 2
+#define T64_NW 6
+#define T64_MINB 2
+#endif
+#ifndef T96_NRB
+#define T96_NRB 16
+#define T96_CTW 1
+#define T96_NW 6
+#define T96_MINB 2
+#endif
+#ifndef T128_CTW
+#define T128_CTW 1
+#define T128_NW 6
+#define T128_MINB 2
+#endif
+#define T64_CFG T64_CTW, T64_NW, T64_MINB
+#define T96_CFG T96_CTW, T96_NW, T96_MINB
+#define T128_CFG T128_CTW, T128_NW, T128_MINB
+
+template <int NRB, int CTW, int NW, int MINB, bool VOXEL>
 static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int m_max,
                        int mm, cudaStream_t s) {
     if (num_items <= 0) return VX_OK;
@@ -2567,11 +2589,11 @@ static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     const int MC = m_max + 1 > PCOLS ? m_max + 1 : PCOLS;
     const TileLayout lay(NRB * 8, mm, MC, m_max, VOXEL);
     const size_t smem = size_t(lay.total) * sizeof(double);
-    auto kfn = gpr_tile_kernel<NRB, CTW, NW, VOXEL>;
+    auto kfn = gpr_tile_kernel<NRB, CTW, NW, MINB, VOXEL>;
     VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = int((size_t(227) * 1024) / (smem + 1024));
+    int per_sm = 0;       // resident CTAs (registers and shared memory): the grid is persistent
+    VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NW * 32, smem));
     if (per_sm < 1) per_sm = 1;
-    if (per_sm > 8) per_sm = 8;
 #ifdef VX_PHASE_TIMING
     if (getenv("VX_TILE_PER_SM")) per_sm = atoi(getenv("VX_TILE_PER_SM"));
 #endif
@@ -2744,12 +2766,12 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         case 0: return launch_wdmma<16>(a, mm, s);
         case 1: return launch_wdmma<24>(a, mm, s);
         case 5: return launch_wdmma<32>(a, mm, s);
-        case 2:   // 32 < n <= 64: two 6-warp CTAs per SM, 2 x 8 right-hand sides per warp
-            return launch_tile<8, 2, 6, true>(a, none, a.num_items, a.M, mm, s);
-        case 6:   // 64 < n <= 96: the n <= 128 kernel (rows beyond n skipped)
-            return launch_tile<16, 1, 6, true>(a, none, a.num_items, a.M, mm, s);
+        case 2:   // 32 < n <= 64
+            return launch_tile<8, T64_CFG, true>(a, none, a.num_items, a.M, mm, s);
+        case 6:   // 64 < n <= 96
+            return launch_tile<T96_NRB, T96_CFG, true>(a, none, a.num_items, a.M, mm, s);
         case 3:   // 96 < n <= 128: two CTAs per SM, one 8-column tile per warp per pass
-            return launch_tile<16, 1, 6, true>(a, none, a.num_items, a.M, mm, s);
+            return launch_tile<16, T128_CFG, true>(a, none, a.num_items, a.M, mm, s);
         case 7:   // 128 < n <= 160
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n < 160 ? max_n : 160,
                                                            a.M, mm, work, s);
@@ -2771,9 +2793,9 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
         if (bucket == 0) return launch_warp<16, false>(none, pa, count, max_m, 1, s);
         if (bucket == 1) return launch_warp<24, false>(none, pa, count, max_m, 1, s);
         if (bucket == 5) return launch_warp<32, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 2) return launch_tile<8, 2, 6, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 6) return launch_tile<16, 1, 6, false>(none, pa, count, max_m, 1, s);
-        if (bucket == 3) return launch_tile<16, 1, 6, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 2) return launch_tile<8, T64_CFG, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 6) return launch_tile<T96_NRB, T96_CFG, false>(none, pa, count, max_m, 1, s);
+        if (bucket == 3) return launch_tile<16, T128_CFG, false>(none, pa, count, max_m, 1, s);
 
         return launch_big<12, false>(none, pa, count, max_n, max_m, 1, work, s);
     }
