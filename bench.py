@@ -228,6 +228,44 @@ def run_trajectory(args, dev):
             "points_per_scan": float(np.mean([len(f[0]) for f in frames]))}
 
 
+def run_scans(args):
+    """Configs 1 and 3: ms per single scan into an empty map, end to end.
+
+    Each repetition resets the map and ingests one scan through the public
+    host API (`MappingEngine.ingest`: copy into pinned staging, H2D of the
+    points, colours and a 640x480 image, hash -> densify -> Gaussian init,
+    ingest report read back), timed on the host (the call synchronises on the
+    report); median of `reps` after warm-up.  These scans (50k / 34k points)
+    are launch-latency bound, the reason the roofline is quoted on config 4.
+    """
+    import torch
+    import paper_2410_17084_b200 as vx
+    sc = scenes.OutdoorScene.make(0)
+    pin = scenes.camera_for(0, 640, 480, 400.0)
+    img = scenes.render_image(sc, pin)
+    cam = vx.Camera(pin.fx, pin.fy, pin.cx, pin.cy, pin.width, pin.height, pin.R, pin.t)
+    out = {}
+    for name, fn, label in (("config1", scenes.config1_scan, "32-beam line-scan"),
+                            ("config3", scenes.config3_scan, "Livox-style rosette")):
+        pos, col = fn(seed=0, frame=0)
+        eng = vx.MappingEngine(vx.PipelineConfig(voxel_size=0.5))
+        times, rep = [], None
+        for i in range(5 + args.scan_reps):
+            eng.reset()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep = eng.ingest(pos, col, cam, img)
+            dt = time.perf_counter() - t0
+            if i >= 5:
+                times.append(dt * 1e3)
+        out[name] = {"workload": f"{name}: one {label} scan ({len(pos)} points, 0.5 m voxels) "
+                                 f"into an empty map, H2D + ingest + report D2H",
+                     "ms_per_scan": float(np.median(times)), "ms_p90": float(np.percentile(times, 90)),
+                     "points": len(pos), "voxels_solved": int(rep.voxels_solved),
+                     "gaussians": int(rep.primitives_added)}
+    return out
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -366,6 +404,7 @@ def run_gpu(args, rank, world, local_rank):
     traj = None
     if args.traj_scans > 0:
         traj = run_trajectory(args, dev)
+    scans = run_scans(args) if args.scan_reps > 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -398,6 +437,7 @@ def run_gpu(args, rank, world, local_rank):
                            "overlapped with frame i)"},
             "gpu_launches": launches,
             "trajectory": traj,
+            "scans": scans,
             "clocks": clk,
             "peaks": {"fp64_tflops_measured": peak64, "hbm_gbs": peaks.get("hbm_gbs")},
         }
@@ -414,6 +454,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--traj-scans", type=int, default=20)
+    ap.add_argument("--scan-reps", type=int, default=20)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
