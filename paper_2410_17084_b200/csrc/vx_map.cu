@@ -154,7 +154,7 @@ __global__ void k_rank_slots(const int32_t* pslot, const int32_t* flags, const i
 }
 
 __global__ void k_point_rank(const int32_t* pslot, const int32_t* trank, int64_t n, uint32_t U,
-                             uint32_t* prank, uint32_t* pidx, int32_t* tcnt) {
+                             uint32_t* prank, int32_t* tcnt) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int32_t s = pslot[i];
@@ -164,7 +164,6 @@ __global__ void k_point_rank(const int32_t* pslot, const int32_t* trank, int64_t
         atomicAdd(tcnt + r, 1);
     }
     prank[i] = r;
-    pidx[i] = uint32_t(i);
 }
 
 __device__ __forceinline__ int32_t grow_cap(int64_t need) {
@@ -580,13 +579,13 @@ static int map_store_frame_impl(VxMap* m, const double* xyz, const double* rgb, 
                                          m->tslot.as<int32_t>(), m->tcnt.as<int32_t>());
     count_launch();
     k_point_rank<<<nblk(n), 256, 0, s>>>(m->pslot.as<int32_t>(), m->trank.as<int32_t>(), n,
-                                         uint32_t(U), m->prank.as<uint32_t>(), m->pidx.as<uint32_t>(),
-                                         m->tcnt.as<int32_t>());
+                                         uint32_t(U), m->prank.as<uint32_t>(), m->tcnt.as<int32_t>());
     count_launch();
     VX_CHECK_LAUNCH();
     bool in_alt = false;
     VX_TRY(radix_sort_pairs(m->prank.as<uint32_t>(), m->pidx.as<uint32_t>(), m->prank2.as<uint32_t>(),
-                            m->pidx2.as<uint32_t>(), n, bits_for(U), m->sort_tmp, s, &in_alt));
+                            m->pidx2.as<uint32_t>(), n, bits_for(U), m->sort_tmp, s, &in_alt,
+                            /*vals_identity=*/true));
     const uint32_t* srank = in_alt ? m->prank2.as<uint32_t>() : m->prank.as<uint32_t>();
     const uint32_t* sidx = in_alt ? m->pidx2.as<uint32_t>() : m->pidx.as<uint32_t>();
     VX_TRY(scan_exclusive_i32(m->tcnt.as<int32_t>(), m->tseg.as<int32_t>(), U,

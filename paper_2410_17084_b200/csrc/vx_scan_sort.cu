@@ -156,53 +156,98 @@ __global__ void __launch_bounds__(RS_T) rs_hist(const uint32_t* keys, int64_t n,
     for (int d = threadIdx.x; d < radix; d += RS_T) hist[int64_t(d) * tiles + blockIdx.x] = h[d];
 }
 
+// Stable scatter of one tile: keys are ranked in (round, warp, lane) order
+// into a shared-memory copy of the tile grouped by digit, which is then
+// written out run by run (consecutive threads -> consecutive addresses of a
+// digit's run) instead of 2-element fragments per digit per round.
 __global__ void __launch_bounds__(RS_T) rs_scatter(const uint32_t* keys, const uint32_t* vals,
                                                    uint32_t* okeys, uint32_t* ovals, int64_t n,
                                                    int shift, int radix, int64_t tiles,
-                                                   const int32_t* offs) {
+                                                   const int32_t* offs, const int32_t* hist) {
+    __shared__ uint32_t sk[RS_TILE];
+    __shared__ uint32_t sv[RS_TILE];
     __shared__ int32_t run[256];
+    __shared__ int32_t gdelta[256];
     __shared__ int32_t wcnt[RS_T / 32][256];
+    __shared__ int32_t wsum[RS_T / 32];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int d = threadIdx.x; d < radix; d += RS_T) {
-        run[d] = offs[int64_t(d) * tiles + blockIdx.x];
-        for (int ww = 0; ww < RS_T / 32; ++ww) wcnt[ww][d] = 0;
+    // local exclusive scan of this tile's digit counts (radix <= 256 = RS_T)
+    const int32_t c = threadIdx.x < radix ? hist[int64_t(threadIdx.x) * tiles + blockIdx.x] : 0;
+    int32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    for (int ww = 0; ww < RS_T / 32; ++ww) wcnt[ww][threadIdx.x] = 0;
+    __syncthreads();
+    int32_t woff = 0;
+    for (int ww = 0; ww < w; ++ww) woff += wsum[ww];
+    if (threadIdx.x < radix) {
+        const int32_t ls = woff + x - c;
+        run[threadIdx.x] = ls;
+        gdelta[threadIdx.x] = offs[int64_t(threadIdx.x) * tiles + blockIdx.x] - ls;
     }
     __syncthreads();
     const int64_t base = int64_t(blockIdx.x) * RS_TILE;
+    const int tn = int(n - base < RS_TILE ? n - base : RS_TILE);
     const uint32_t mask = uint32_t(radix - 1);
     for (int k = 0; k < RS_ROUNDS; ++k) {
-        const int64_t i = base + int64_t(k) * RS_T + threadIdx.x;
-        const bool valid = i < n;
-        uint32_t key = valid ? keys[i] : 0u;
-        int d = valid ? int((key >> shift) & mask) : 256 + lane;   // unique dummy digits
-        unsigned peers = __match_any_sync(FULL, d);
-        int lrank = __popc(peers & lanemask_lt());
+        const int li = k * RS_T + threadIdx.x;
+        const bool valid = li < tn;
+        const uint32_t key = valid ? keys[base + li] : 0u;
+        const uint32_t val = valid ? (vals ? vals[base + li] : uint32_t(base + li)) : 0u;   // null: identity
+        const int d = valid ? int((key >> shift) & mask) : 256 + lane;   // unique dummy digits
+        const unsigned peers = __match_any_sync(FULL, d);
+        const int lrank = __popc(peers & lanemask_lt());
         if (valid && lrank == 0) wcnt[w][d] = __popc(peers);
         __syncthreads();
         if (valid) {
             int off = run[d] + lrank;
             for (int ww = 0; ww < w; ++ww) off += wcnt[ww][d];
-            okeys[off] = key;
-            ovals[off] = vals[i];
+            sk[off] = key;
+            sv[off] = val;
         }
         __syncthreads();
-        for (int dd = threadIdx.x; dd < radix; dd += RS_T) {
+        if (threadIdx.x < radix) {
             int tot = 0;
 #pragma unroll
             for (int ww = 0; ww < RS_T / 32; ++ww) {
-                tot += wcnt[ww][dd];
-                wcnt[ww][dd] = 0;
+                tot += wcnt[ww][threadIdx.x];
+                wcnt[ww][threadIdx.x] = 0;
             }
-            run[dd] += tot;
+            run[threadIdx.x] += tot;
         }
         __syncthreads();
     }
+    for (int j = threadIdx.x; j < tn; j += RS_T) {
+        const uint32_t key = sk[j];
+        const int64_t g = int64_t(gdelta[(key >> shift) & mask]) + j;
+        okeys[g] = key;
+        ovals[g] = sv[j];
+    }
 }
 
+__global__ void rs_iota(uint32_t* v, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = uint32_t(i);
+}
+
+// vals_identity: the values are 0..n-1 and `vals` is only written (the first
+// pass generates them instead of reading an iota array)
 int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                     int64_t n, int bits, DevBuf& tmp, cudaStream_t s, bool* result_in_alt) {
+                     int64_t n, int bits, DevBuf& tmp, cudaStream_t s, bool* result_in_alt,
+                     bool vals_identity) {
     *result_in_alt = false;
-    if (n <= 1 || bits <= 0) return VX_OK;
+    if (n <= 1 || bits <= 0) {
+        if (vals_identity && n > 0) {
+            rs_iota<<<unsigned((n + 255) / 256), 256, 0, s>>>(vals, n);
+            count_launch();
+            VX_CHECK_LAUNCH();
+        }
+        return VX_OK;
+    }
     const int passes = (bits + 7) / 8;
     const int dbits = (bits + passes - 1) / passes;
     const int radix = 1 << dbits;
@@ -221,7 +266,8 @@ int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_
         VX_CHECK_LAUNCH();
         VX_TRY(scan_exclusive<int32_t>(hist, offs, hn, nullptr, tmp, s,
                                        (hist_bytes + 255) & ~size_t(255)));
-        rs_scatter<<<unsigned(tiles), RS_T, 0, s>>>(ik, iv, ok, ov, n, shift, radix, tiles, offs);
+        rs_scatter<<<unsigned(tiles), RS_T, 0, s>>>(ik, (p == 0 && vals_identity) ? nullptr : iv, ok, ov,
+                                                    n, shift, radix, tiles, offs, hist);
         count_launch();
         VX_CHECK_LAUNCH();
         uint32_t* t;
@@ -231,5 +277,4 @@ int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_
     }
     return VX_OK;
 }
-
 }  // namespace vx

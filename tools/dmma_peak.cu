@@ -39,6 +39,36 @@ __global__ void k_dfma(double* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// half the warps issue DMMA chains, the other half DFMA chains: do the two
+// FP64 pipes add up?
+__global__ void k_mixed(double* out, int iters) {
+    const int w = threadIdx.x >> 5;
+    double s = 0;
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+    if (w & 1) {
+        double c[8][2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    } else {
+        double c[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i] = i;
+        for (int it = 0; it < 16 * iters; ++it) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) c[i] = fma(a, c[i], b);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += c[i];
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename K>
 float time_it(K kern, int blocks, int threads, double* out, int iters) {
     cudaEvent_t e0, e1;
@@ -75,6 +105,14 @@ int main() {
         float ms = time_it(k_dfma<8>, sms, 32 * wps, out, iters);
         double flops = double(sms) * 32 * wps * iters * 8 * 2.0;
         printf("DFMA  %2d warps/SM x 8 chains: %7.2f TFLOP/s\n", wps, flops / ms / 1e9);
+    }
+    for (int wps : {8, 16}) {
+        float ms = time_it(k_mixed, sms, 32 * wps, out, iters / 4);
+        // wps/2 DMMA warps x 8 chains x 512 flops, wps/2 DFMA warps x 16 x 8 chains x 64 flops
+        double fl_dmma = double(sms) * (wps / 2) * (iters / 4) * 8 * 512.0;
+        double fl_dfma = double(sms) * (wps / 2) * (iters / 4) * 16 * 8 * 64.0;
+        printf("MIXED %2d warps/SM: %7.2f TFLOP/s total (DMMA share %.2f)\n", wps,
+               (fl_dmma + fl_dfma) / ms / 1e9, fl_dmma / (fl_dmma + fl_dfma));
     }
     return 0;
 }
