@@ -30,7 +30,7 @@ buckets = [("gpr_big_kernel<12", (128, 160), "gpr_n160"),
            ("gpr_wdmma_kernel<32", (24, 32), "gpr_n32"),
            ("gpr_big_kernel<12", (160, 10 ** 9), "gpr_n_large"),
            ("gpr_tile_kernel<16, 1, 6", (96, 128), "gpr_n128"),
-           ("gpr_tile_kernel<8, 2, 6", (32, 64), "gpr_n64"),
+           ("gpr_tile_kernel<8,", (32, 64), "gpr_n64"),
            ("gpr_wdmma_kernel<24", (16, 24), "gpr_n24"),
            ("gpr_wdmma_kernel<16", (0, 16), "gpr_n16")]
 res = {}
