@@ -1687,6 +1687,31 @@ __device__ __forceinline__ void team_fill_matrix(double* L, const int* CO, const
     }
 }
 
+// A = K + diag(noise) (+ jitter) for one 8x8 tile (rows 8t.., block column
+// kb) by one warp, two entries per lane (lane = row-major entry): the fill of
+// block column kb+1 runs in the shadow of panel kb's factorisation chain.
+__device__ __forceinline__ void warp_fill_tile(double* L, const int* CO, const double* X,
+                                               const double* NZ, int n, int t, int kb, int kind,
+                                               double lam, double jit, int lane) {
+    double v[2];
+    int dst[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int e = lane + 32 * u;
+        const int i = 8 * t + (e >> 3), j = 8 * kb + (e & 7);
+        const int ic = i < n ? i : 0, jc = j < n ? j : 0;
+        const double kv = kernel_value(kind, lam, dist2_exact(X[2 * ic], X[2 * ic + 1],
+                                                              X[2 * jc], X[2 * jc + 1]));
+        double dg = xadd(1.0, NZ[ic]);
+        if (jit != 0.0) dg = xadd(dg, jit);
+        v[u] = (i >= n || j >= n) ? (i == j ? 1.0 : 0.0) : (i == j ? dg : kv);
+        dst[u] = j <= i ? CO[j] + i : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+        if (dst[u] >= 0) L[dst[u]] = v[u];
+}
+
 // Cholesky update of the 8x8 tile (rows 8t.., panel columns jp..jp+7):
 // A -= L(rows, k_lo:k_hi) L(panel, k_lo:k_hi)^T with DMMA; k_lo, k_hi are
 // multiples of 8 and the two k-chunks of each block column feed separate
@@ -1952,6 +1977,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs 
     constexpr int N8 = NRB * 8;
     constexpr int NT = NW * 32;
     constexpr int PCOLS = NW * CTW * 8;             // right-hand sides per pass
+    constexpr bool INC_FILL = NW >= 6;              // fill block columns in the chain's shadow
     const int MC = mmax + 1 > PCOLS ? mmax + 1 : PCOLS;   // columns of [f | K*] (padded)
     const TileLayout lay(N8, mm, MC, mmax, VOXEL);
     double* L = smem + lay.L;
@@ -2033,7 +2059,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs 
         bool ok = false;
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? jitter : 0.0;
-            team_fill_matrix(L, CO, X, NZ, n, n8, kind, lam, jit, tid, NT);
+            // INC_FILL: block column 0 now; block column kb+1 is filled during
+            // panel kb by the warps that do not factor (below), before their
+            // look-ahead (measured: n > 64 buckets 6-7% faster; with 4 warps the
+            // idle warps are too few and the up-front fill wins)
+            if constexpr (INC_FILL)
+                for (int t = warp; t < nrb; t += NW) warp_fill_tile(L, CO, X, NZ, n, t, 0, kind, lam, jit, lane);
+            else
+                team_fill_matrix(L, CO, X, NZ, n, n8, kind, lam, jit, tid, NT);
             __syncthreads();
             VX_PHASE(1, tph);                 // kernel matrix
             ok = true;
@@ -2061,12 +2094,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs 
                 // two.  The other warps meanwhile apply every final column (< j0) to
                 // the NEXT panel (look-ahead), hiding the serial factorisation.
                 const int below = n8 - j0 - 8;
-                const int nfw = below > 32 ? (below + 31) / 32 : 1;
+                int nfw = below > 32 ? (below + 31) / 32 : 1;
+                if (nfw >= NW) nfw = NW - 1;          // keep a warp for the fill of the next block column
                 const bool la = (kb + 1 < nrb) && (NW > nfw) && j0 > 0;
                 if (warp >= nfw) {
-                    if (la)
-                        for (int t = kb + 1 + (warp - nfw); t < nrb; t += NW - nfw)
-                            tile_update(t, j0 + 8, 0, j0);
+                    for (int t = kb + 1 + (warp - nfw); t < nrb; t += NW - nfw) {
+                        if constexpr (INC_FILL) {
+                            warp_fill_tile(L, CO, X, NZ, n, t, kb + 1, kind, lam, jit, lane);
+                            __syncwarp();
+                        }
+                        if (la) tile_update(t, j0 + 8, 0, j0);
+                    }
                 } else {
                     chol_diag_and_rows(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
                 }
@@ -2364,7 +2402,13 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
         bool ok = false;
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? jitter : 0.0;
-            team_fill_matrix(L, CO, X, NZ, n, n8, kind, lam, jit, tid, NT);
+            // shared-memory variant (n <= ~160): block column 0 now, block column
+            // kb+1 during panel kb (as the tile kernel); larger n fill up front
+            // (too few idle warps next to the long early panels)
+            if constexpr (SMEM)
+                for (int t = warp; t < nrb; t += NW) warp_fill_tile(L, CO, X, NZ, n, t, 0, kind, lam, jit, lane);
+            else
+                team_fill_matrix(L, CO, X, NZ, n, n8, kind, lam, jit, tid, NT);
             __syncthreads();
             ok = true;
             // DMMA update of one 8x8 row tile of panel `jp` with columns [k_lo, k_hi)
@@ -2387,12 +2431,17 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
                 // two.  The other warps meanwhile apply every final column (< j0) to
                 // the NEXT panel (look-ahead), hiding the serial factorisation.
                 const int below = n8 - j0 - 8;
-                const int nfw = below > 32 ? (below + 31) / 32 : 1;
+                int nfw = below > 32 ? (below + 31) / 32 : 1;
+                if (SMEM && nfw >= NW) nfw = NW - 1;  // keep a warp for the fill of the next block column
                 const bool la = (kb + 1 < nrb) && (NW > nfw) && j0 > 0;
                 if (warp >= nfw) {
-                    if (la)
-                        for (int t = kb + 1 + (warp - nfw); t < nrb; t += NW - nfw)
-                            tile_update(t, j0 + 8, 0, j0);
+                    for (int t = kb + 1 + (warp - nfw); t < nrb; t += NW - nfw) {
+                        if constexpr (SMEM) {
+                            warp_fill_tile(L, CO, X, NZ, n, t, kb + 1, kind, lam, jit, lane);
+                            __syncwarp();
+                        }
+                        if (la) tile_update(t, j0 + 8, 0, j0);
+                    }
                 } else {
                     chol_diag_and_rows(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
                 }
