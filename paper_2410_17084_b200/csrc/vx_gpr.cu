@@ -1740,6 +1740,7 @@ __device__ __forceinline__ void chol_tile_update(double* L, const int* CO, int n
 // same operation order as the column-oriented substitution.  Thread 0
 // publishes the factored block (LDG, row-major), 1/L_jj (INV) and the pivot
 // flag (0 when a pivot is <= 0 or NaN, the dpotrf failure rule).
+template <bool TWO>
 __device__ __forceinline__ void chol_diag_and_rows(double* L, const int* CO, double* LDG,
                                                    double* INV, double* flag, int j0, int n8,
                                                    int tid, int nft) {
@@ -1794,19 +1795,33 @@ __device__ __forceinline__ void chol_diag_and_rows(double* L, const int* CO, dou
         if (tid == 0) *flag = ok ? 1.0 : 0.0;
     }
     VX_PHASE(8, tp);                                // publish
-    for (int i = j0 + 8 + tid; i < n8; i += nft) {
-        double v[8];
+    // TWO: two rows per thread per iteration (independent chains interleaved)
+    for (int i = j0 + 8 + tid; i < n8; i += (TWO ? 2 : 1) * nft) {
+        const bool two = TWO && i + nft < n8;
+        double v[8], u[8];
         double* row = blk + (i - j0);
+        double* row2 = row + (two ? nft : 0);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = row[c * ldb];
+        for (int c = 0; c < 8; ++c) {
+            v[c] = row[c * ldb];
+            if (TWO) u[c] = row2[c * ldb];
+        }
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             v[c] *= inv[c];
+            if (TWO) u[c] *= inv[c];
 #pragma unroll
-            for (int k = c + 1; k < 8; ++k) v[k] = fma(-v[c], a[k * (k + 1) / 2 + c], v[k]);
+            for (int k = c + 1; k < 8; ++k) {
+                v[k] = fma(-v[c], a[k * (k + 1) / 2 + c], v[k]);
+                if (TWO) u[k] = fma(-u[c], a[k * (k + 1) / 2 + c], u[k]);
+            }
         }
 #pragma unroll
         for (int c = 0; c < 8; ++c) row[c * ldb] = v[c];
+        if (two) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) row2[c * ldb] = u[c];
+        }
     }
     VX_PHASE(9, tp);                                // rows below
 }
@@ -1970,7 +1985,7 @@ __device__ void team_voxel_epilogue(const VoxelSolveArgs& va, const VoxelCtx& c,
     }
 }
 
-template <int NRB, int CTW, int NW, int MINB, bool VOXEL>
+template <int NRB, int CTW, int NW, int MINB, int ROWS, bool VOXEL>
 __global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
                                                            int mmax, int mm) {
     extern __shared__ __align__(16) double smem[];
@@ -2094,7 +2109,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs 
                 // two.  The other warps meanwhile apply every final column (< j0) to
                 // the NEXT panel (look-ahead), hiding the serial factorisation.
                 const int below = n8 - j0 - 8;
-                int nfw = below > 32 ? (below + 31) / 32 : 1;
+                // ROWS = 2: the factor warps solve two rows per thread, so more
+                // warps are free for the fill and look-ahead of the next block
+                // column (balances the two paths of a panel for n > 96)
+                int nfw = ROWS == 2 ? (below > 64 ? (below + 63) / 64 : 1) : (below > 32 ? (below + 31) / 32 : 1);
                 if (nfw >= NW) nfw = NW - 1;          // keep a warp for the fill of the next block column
                 const bool la = (kb + 1 < nrb) && (NW > nfw) && j0 > 0;
                 if (warp >= nfw) {
@@ -2106,7 +2124,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs 
                         if (la) tile_update(t, j0 + 8, 0, j0);
                     }
                 } else {
-                    chol_diag_and_rows(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
+                    chol_diag_and_rows<ROWS == 2>(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
                 }
 #ifdef VX_PHASE_TIMING
                 tsub = clock64();
@@ -2443,7 +2461,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
                         if (la) tile_update(t, j0 + 8, 0, j0);
                     }
                 } else {
-                    chol_diag_and_rows(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
+                    chol_diag_and_rows<false>(L, CO, LDG, INV, smem + lay.FLAG, j0, n8, tid, (nfw < NW ? nfw : NW) * 32);
                 }
                 __syncthreads();
                 la_prev = la;
@@ -2609,28 +2627,32 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
 }
 
 // tile-kernel configurations per size bucket: (8-column tiles per warp and
-// pass, warps per CTA, resident CTAs per SM the registers are capped for)
+// pass, warps per CTA, resident CTAs per SM the registers are capped for,
+// rows per factor thread in the panel solve)
 #ifndef T64_CTW
 #define T64_CTW 1             // four 4-warp CTAs per SM (measured: 4.55 -> 4.02 ms vs two 6-warp CTAs)
 #define T64_NW 4
 #define T64_MINB 4
+#define T64_ROWS 1
 #endif
 #ifndef T96_NRB
 #define T96_NRB 16
 #define T96_CTW 1
 #define T96_NW 6
 #define T96_MINB 2
+#define T96_ROWS 1
 #endif
 #ifndef T128_CTW
 #define T128_CTW 1
 #define T128_NW 6
 #define T128_MINB 2
+#define T128_ROWS 2           // two rows per factor thread (measured: 8.60 -> 8.29 ms)
 #endif
-#define T64_CFG T64_CTW, T64_NW, T64_MINB
-#define T96_CFG T96_CTW, T96_NW, T96_MINB
-#define T128_CFG T128_CTW, T128_NW, T128_MINB
+#define T64_CFG T64_CTW, T64_NW, T64_MINB, T64_ROWS
+#define T96_CFG T96_CTW, T96_NW, T96_MINB, T96_ROWS
+#define T128_CFG T128_CTW, T128_NW, T128_MINB, T128_ROWS
 
-template <int NRB, int CTW, int NW, int MINB, bool VOXEL>
+template <int NRB, int CTW, int NW, int MINB, int ROWS, bool VOXEL>
 static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_items, int m_max,
                        int mm, cudaStream_t s) {
     if (num_items <= 0) return VX_OK;
@@ -2638,7 +2660,7 @@ static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     const int MC = m_max + 1 > PCOLS ? m_max + 1 : PCOLS;
     const TileLayout lay(NRB * 8, mm, MC, m_max, VOXEL);
     const size_t smem = size_t(lay.total) * sizeof(double);
-    auto kfn = gpr_tile_kernel<NRB, CTW, NW, MINB, VOXEL>;
+    auto kfn = gpr_tile_kernel<NRB, CTW, NW, MINB, ROWS, VOXEL>;
     VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;       // resident CTAs (registers and shared memory): the grid is persistent
     VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NW * 32, smem));
