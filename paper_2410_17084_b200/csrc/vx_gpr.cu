@@ -1780,21 +1780,7 @@ __device__ __forceinline__ void chol_diag_and_rows(double* L, const int* CO, dou
     if (tid == 0) { const double s1 = a[35] + inv[7]; asm volatile("" :: "d"(s1)); }
 #endif
     VX_PHASE(7, tp);                                // factorisation chain
-    if (tid < 8) {                                  // thread r publishes row r (selects, no local array)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            double v = 0.0;
-#pragma unroll
-            for (int rr = k; rr < 8; ++rr) v = tid == rr ? a[rr * (rr + 1) / 2 + k] : v;
-            LDG[(j0 + tid) * 8 + k] = v;
-        }
-        double iv = inv[0];
-#pragma unroll
-        for (int c = 1; c < 8; ++c) iv = tid == c ? inv[c] : iv;
-        INV[j0 + tid] = iv;
-        if (tid == 0) *flag = ok ? 1.0 : 0.0;
-    }
-    VX_PHASE(8, tp);                                // publish
+    VX_PHASE(8, tp);                                // (publish: after the rows)
     // TWO: two rows per thread per iteration (independent chains interleaved)
     for (int i = j0 + 8 + tid; i < n8; i += (TWO ? 2 : 1) * nft) {
         const bool two = TWO && i + nft < n8;
@@ -1823,7 +1809,18 @@ __device__ __forceinline__ void chol_diag_and_rows(double* L, const int* CO, dou
             for (int c = 0; c < 8; ++c) row2[c * ldb] = u[c];
         }
     }
-    VX_PHASE(9, tp);                                // rows below
+    // publish the factored block (lower part of LDG rows), 1/L_jj and the pivot
+    // flag: static register indices by one thread, off the row-solve path
+    if (tid == 0) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c <= r; ++c) LDG[(j0 + r) * 8 + c] = a[r * (r + 1) / 2 + c];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) INV[j0 + c] = inv[c];
+        *flag = ok ? 1.0 : 0.0;
+    }
+    VX_PHASE(9, tp);                                // rows below + publish
 }
 
 // ---------------------------------------------------------------------------
