@@ -313,6 +313,28 @@ int vx_decode_ply(const void* d_records, int64_t n, double* d_xyz, double* d_rgb
 int vx_pack_map_records(const VxGaussianOut* records, int64_t count, void* d_out, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Forward splat renderer (renderer.py): the consumer of
+ * the Gaussian records.  Primitives are SoA device arrays: position (n,3),
+ * scale (n,3), rotation (n,4) w-first, opacity (n), SH0 colour (n,3).
+ * ---------------------------------------------------------------------- */
+/* project_points (renderer.py:90-137): mean2d (n,2) pixels, cov2d (n,4)
+ * row-major 2x2 with the 0.3 px^2 dilation, camera depth (n), 3-sigma radius
+ * (n), valid (n) u8 (in front of near_plane, bbox on the image), bbox (n,4)
+ * int64 half-open x0,x1,y0,y1 (zero when invalid). */
+int vx_project_points(const double* d_pos, const double* d_scale, const double* d_rot, int64_t n,
+                      const VxCamera* camera, double near_plane, double* d_mean2d, double* d_cov2d,
+                      double* d_depth, double* d_radius, uint8_t* d_valid, int64_t* d_bbox,
+                      void* stream);
+
+/* render (renderer.py:184-207): front-to-back alpha blending of the valid
+ * primitives (global depth order, ties by index) into colour (H,W,3), depth
+ * (H,W) and silhouette (H,W), composited over black; 16x16-pixel tiles,
+ * one CTA per tile. */
+int vx_render(const double* d_pos, const double* d_scale, const double* d_rot, const double* d_opacity,
+              const double* d_sh0, int64_t n, const VxCamera* camera, double near_plane,
+              double* d_color, double* d_depth, double* d_silhouette, void* stream);
+
+/* ------------------------------------------------------------------------
  * Measurement helper: FP64 FMA peak of this device (DFMA chains, all SMs).
  * ---------------------------------------------------------------------- */
 int vx_fp64_peak(double* tflops, void* stream);

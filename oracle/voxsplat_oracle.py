@@ -438,3 +438,89 @@ def ingest(omap: OracleMap, positions, colors, cfg: DensifyConfig,
                     **splat))
     return {"update": update, "predictions": preds, "skipped": skipped,
             "gaussians": gauss}
+
+
+# ---------------------------------------------------------------------------
+# Forward splat renderer (renderer.py:90-207) — restated per primitive in a
+# plain loop over pixels of its bbox rows (no patch broadcasting), checked
+# against the reference's own outputs (tests/golden/render.npz).
+# ---------------------------------------------------------------------------
+R_ALPHA_CEILING, R_ALPHA_SKIP, R_T_EPS = 0.99, 1.0 / 255.0, 1e-4      # renderer.py:27-29
+R_DILATION, R_SIGMAS = 0.3, 3.0                                       # renderer.py:30-31
+
+
+def quat_rotation(q):
+    """Rotation of a w-first quaternion, normalised first (geometry.py:34-48)."""
+    w, x, y, z = np.asarray(q, dtype=float) / np.linalg.norm(q)
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+def project_splats(pos, scl, rot, cam, near=0.01):
+    """Per-primitive projection (renderer.py:90-137): mean2d, cov2d, depth,
+    radius, valid, bbox — one primitive at a time."""
+    fx, fy, cx, cy, W, H = cam["fx"], cam["fy"], cam["cx"], cam["cy"], cam["width"], cam["height"]
+    Rc, t = np.asarray(cam["R"], dtype=float), np.asarray(cam["t"], dtype=float)
+    n = len(pos)
+    out = dict(mean2d=np.zeros((n, 2)), cov2d=np.zeros((n, 2, 2)), depth=np.zeros(n),
+               radius=np.zeros(n), valid=np.zeros(n, dtype=bool), bbox=np.zeros((n, 4), np.int64))
+    for i in range(n):
+        pc = Rc @ np.asarray(pos[i], dtype=float) + t
+        x, y, z = pc
+        ok = z > near
+        zs = z if ok else 1.0
+        u, v = fx * x / zs + cx, fy * y / zs + cy
+        G = quat_rotation(rot[i])
+        phi = G @ np.diag(np.asarray(scl[i], dtype=float) ** 2) @ G.T
+        M = Rc @ phi @ Rc.T
+        J = np.array([[fx / zs, 0.0, -fx * x / zs ** 2], [0.0, fy / zs, -fy * y / zs ** 2]])
+        c2 = J @ M @ J.T + R_DILATION * np.eye(2)
+        c2 = 0.5 * (c2 + c2.T)
+        a, b, c = c2[0, 0], c2[0, 1], c2[1, 1]
+        lam = 0.5 * (a + c) + math.sqrt(max((0.5 * (a - c)) ** 2 + b * b, 0.0))
+        rad = R_SIGMAS * math.sqrt(max(lam, 0.0))
+        ok = ok and u + rad >= 0 and u - rad <= W - 1 and v + rad >= 0 and v - rad <= H - 1
+        ok = ok and math.isfinite(u) and math.isfinite(v)
+        x0 = int(min(max(math.ceil(u - rad), 0), W)) if math.isfinite(u) else 0
+        x1 = int(min(max(math.floor(u + rad) + 1, 0), W)) if math.isfinite(u) else 0
+        y0 = int(min(max(math.ceil(v - rad), 0), H)) if math.isfinite(v) else 0
+        y1 = int(min(max(math.floor(v + rad) + 1, 0), H)) if math.isfinite(v) else 0
+        ok = ok and x1 > x0 and y1 > y0
+        out["mean2d"][i] = (u, v)
+        out["cov2d"][i] = c2
+        out["depth"][i] = z
+        out["radius"][i] = rad
+        out["valid"][i] = ok
+        if ok:
+            out["bbox"][i] = (x0, x1, y0, y1)
+    return out
+
+
+def render_splats(pos, scl, rot, opacity, sh0, cam, near=0.01):
+    """Front-to-back blending (renderer.py:176-207): colour (H,W,3), depth, silhouette."""
+    pr = project_splats(pos, scl, rot, cam, near)
+    W, H = cam["width"], cam["height"]
+    color, depth, sil = np.zeros((H, W, 3)), np.zeros((H, W)), np.zeros((H, W))
+    T = np.ones((H, W))
+    rgb = np.asarray(sh0, dtype=float) * 0.28209479177 + 0.5
+    idx = np.flatnonzero(pr["valid"])
+    for i in idx[np.argsort(pr["depth"][idx], kind="stable")]:
+        x0, x1, y0, y1 = pr["bbox"][i]
+        m0, m1 = pr["mean2d"][i]
+        a, b, c = pr["cov2d"][i][0, 0], pr["cov2d"][i][0, 1], pr["cov2d"][i][1, 1]
+        det = a * c - b * b
+        dx = np.arange(x0, x1, dtype=float) - m0
+        for py in range(y0, y1):
+            dy = float(py) - m1
+            power = -0.5 * (c * dx ** 2 - 2.0 * b * dx * dy + a * dy ** 2) / det
+            al = np.minimum(opacity[i] * np.exp(power), R_ALPHA_CEILING)
+            al[al < R_ALPHA_SKIP] = 0.0
+            Tr = T[py, x0:x1]
+            live = Tr >= R_T_EPS
+            w = np.where(live, al * Tr, 0.0)
+            color[py, x0:x1] += w[:, None] * rgb[i]
+            depth[py, x0:x1] += w * pr["depth"][i]
+            sil[py, x0:x1] += w
+            T[py, x0:x1] = np.where(live, Tr * (1.0 - al), Tr)
+    return color, depth, sil, pr

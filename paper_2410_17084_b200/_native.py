@@ -125,6 +125,10 @@ _SIGS = {
     "vx_fp64_peak": ([C.POINTER(C.c_double), vp], C.c_int),
     "vx_pack_map_records": ([C.POINTER(VxGaussianOut), C.c_int64, vp, vp], C.c_int),
     "vx_decode_ply": ([vp, C.c_int64, vp, vp, vp], C.c_int),
+    "vx_project_points": ([vp, vp, vp, C.c_int64, C.POINTER(VxCamera), C.c_double, vp, vp, vp, vp,
+                           vp, vp, vp], C.c_int),
+    "vx_render": ([vp, vp, vp, vp, vp, C.c_int64, C.POINTER(VxCamera), C.c_double, vp, vp, vp, vp],
+                  C.c_int),
     "vx_profile": ([C.c_int], C.c_int),
     "vx_profile_read": ([C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32], C.c_int),
 }

@@ -550,6 +550,29 @@ int vx_init_color(const double* d_positions, const double* d_fallback, int64_t n
     return launch_init_color(d_positions, d_fallback, n, *camera, d_image, d_sh0, as_stream(stream));
 }
 
+int vx_project_points(const double* d_pos, const double* d_scale, const double* d_rot, int64_t n,
+                      const VxCamera* camera, double near_plane, double* d_mean2d, double* d_cov2d,
+                      double* d_depth, double* d_radius, uint8_t* d_valid, int64_t* d_bbox,
+                      void* stream) {
+    if (!camera || n < 0) {
+        set_error("project_points: camera required, n >= 0");
+        return VX_E_INPUT;
+    }
+    return project_points(d_pos, d_scale, d_rot, n, *camera, near_plane, d_mean2d, d_cov2d, d_depth,
+                          d_radius, d_valid, d_bbox, as_stream(stream));
+}
+
+int vx_render(const double* d_pos, const double* d_scale, const double* d_rot, const double* d_opacity,
+              const double* d_sh0, int64_t n, const VxCamera* camera, double near_plane,
+              double* d_color, double* d_depth, double* d_silhouette, void* stream) {
+    if (!camera || n < 0 || camera->width <= 0 || camera->height <= 0) {
+        set_error("render: camera with a positive image size required, n >= 0");
+        return VX_E_INPUT;
+    }
+    return render_splats(d_pos, d_scale, d_rot, d_opacity, d_sh0, n, *camera, near_plane, d_color,
+                         d_depth, d_silhouette, as_stream(stream));
+}
+
 int vx_profile(int enable) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     prof_collect();

@@ -129,6 +129,14 @@ int launch_gaussians(const double* pred_xyz, const double* pred_rgb, const doubl
                      const double* image, const VxSplatConfig& cfg, const VxGaussianOut& out,
                      cudaStream_t s);
 int launch_decode_ply(const uint8_t* rec, int64_t n, double* xyz, double* rgb, cudaStream_t s);
+
+// ---------------------------------------------------------------- renderer
+int project_points(const double* pos, const double* scale, const double* rot, int64_t n,
+                   const VxCamera& cam, double near, double* mean2d, double* cov2d, double* depth,
+                   double* radius, uint8_t* valid, int64_t* bbox, cudaStream_t s);
+int render_splats(const double* pos, const double* scale, const double* rot, const double* opacity,
+                  const double* sh0, int64_t n, const VxCamera& cam, double near, double* color,
+                  double* depth, double* sil, cudaStream_t s);
 int launch_pack_records(const VxGaussianOut& in, int64_t count, void* out, cudaStream_t s);
 int launch_moments(const double* pts, const double* w, int64_t G, int k, const double* center,
                    double* pos, double* phi, cudaStream_t s);

@@ -20,6 +20,11 @@ Fixtures
   scan_frames.npz    3-frame mapping replay through MappingPipeline.ingest_frame
                      (pipeline.py:139-187): update order, per-voxel counts,
                      transitions, predictions, Gaussian map
+  render.npz         project_points / render (renderer.py:90-207) on three
+                     scenes: the reference tests' random scene, an
+                     anisotropic rotated scene under a looking_at camera
+                     (incl. behind-camera, off-image, equal-depth and faint
+                     splats), and the Gaussian map of the scan replay
 """
 
 from __future__ import annotations
@@ -248,6 +253,57 @@ def ply_fixture():
     np.savez_compressed(os.path.join(HERE, "ply_ref.npz"), **out)
 
 
+def render_fixture():
+    from voxsplat.renderer import project_points, render
+    from voxsplat.splat_init import GaussianPrimitive, rgb_to_sh0
+    out = {}
+
+    def add(tag, pos, scl, rot, opa, sh0, cam):
+        prims = [GaussianPrimitive(position=pos[i], scale=scl[i], rotation=rot[i] / np.linalg.norm(rot[i]),
+                                   opacity=float(opa[i]), color=sh0[i]) for i in range(len(pos))]
+        buf = render(prims, cam)
+        ps = project_points(pos, scl, rot, cam)
+        for k, v in (("pos", pos), ("scale", scl), ("rot", rot), ("opacity", opa), ("sh0", sh0),
+                     ("color", buf.color), ("depth", buf.depth), ("sil", buf.silhouette),
+                     ("mean2d", ps.mean2d), ("cov2d", ps.cov2d), ("pdepth", ps.depth),
+                     ("radius", ps.radius), ("valid", ps.valid), ("bbox", ps.bbox)):
+            out[f"{tag}_{k}"] = np.asarray(v)
+        out[f"{tag}_cam"] = np.concatenate([[cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height],
+                                            cam.rotation.reshape(-1), cam.translation])
+
+    # (a) the reference tests' random scene (tests/test_renderer.py:76-86)
+    rng = np.random.default_rng(0)
+    n = 30
+    pos = rng.uniform([-0.6, -0.6, 0.8], [0.6, 0.6, 3.0], (n, 3))
+    col = rng.uniform(0, 1, (n, 3))
+    opa = rng.uniform(0.2, 1.0, n)
+    scl = np.repeat(rng.uniform(0.02, 0.15, n)[:, None], 3, axis=1)
+    rot = np.tile([1.0, 0.0, 0.0, 0.0], (n, 1))
+    add("a", pos, scl, rot, opa, rgb_to_sh0(col), Camera(fx=64, fy=64, cx=31.5, cy=31.5, width=64, height=64))
+    # (b) anisotropic, rotated primitives under a looking_at camera
+    rng = np.random.default_rng(5)
+    n = 400
+    pos = rng.uniform([-3, -3, -0.5], [3, 3, 1.5], (n, 3))
+    pos[:5] = [[0, -8, 1], [0, 30, 1], [40, 0, 0], [0.5, 0.5, 0.5], [0.5, 0.5, 0.5]]  # behind, far, off, ties
+    scl = rng.uniform(0.01, 0.4, (n, 3))
+    rot = rng.normal(size=(n, 4))
+    opa = rng.uniform(0.05, 1.0, n)
+    opa[5:10] = 0.5 / 255.0                                   # below the skip threshold
+    sh0 = rgb_to_sh0(rng.uniform(0, 1, (n, 3)))
+    cam = Camera.looking_at((0.3, -6.0, 2.0), (0.0, 0.0, 0.3), fx=80.0, fy=80.0, cx=47.5, cy=35.5,
+                            width=96, height=72)
+    add("b", pos, scl, rot, opa, sh0, cam)
+    # (c) the Gaussian map of the scan replay fixture, seen by its camera
+    sf = np.load(os.path.join(HERE, "scan_frames.npz"))
+    g = {k: np.concatenate([sf[f"f{f}_g_{k}"] for f in range(3)])
+         for k in ("positions", "scales", "rotations", "opacities", "colors")}
+    fx, fy, cx, cy, w, h = sf["camera_intrinsics"]
+    cam = Camera(fx=fx, fy=fy, cx=cx, cy=cy, width=int(w), height=int(h), rotation=sf["f2_R"],
+                 translation=sf["f2_t"])
+    add("c", g["positions"], g["scales"], g["rotations"], g["opacities"], g["colors"], cam)
+    np.savez_compressed(os.path.join(HERE, "render.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -260,6 +316,7 @@ if __name__ == "__main__":
     grids_fixture()
     subgrid_fixture()
     scan_fixture()
+    render_fixture()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

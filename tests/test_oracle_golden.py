@@ -123,3 +123,22 @@ def test_scan_replay_matches_reference():
     np.testing.assert_array_equal(np.array(keys), d["final_keys"])
     np.testing.assert_array_equal([len(omap.cells[k].raw_pos) for k in keys], d["final_counts"])
     np.testing.assert_array_equal([omap.cells[k].state for k in keys], d["final_states"])
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_oracle_renderer_matches_reference_golden(tag):
+    """Renderer restatement vs the reference's render()/project_points()."""
+    g = F.load("render.npz")
+    cv = g[f"{tag}_cam"]
+    cam = dict(fx=cv[0], fy=cv[1], cx=cv[2], cy=cv[3], width=int(cv[4]), height=int(cv[5]),
+               R=cv[6:15].reshape(3, 3), t=cv[15:18])
+    color, depth, sil, pr = O.render_splats(g[f"{tag}_pos"], g[f"{tag}_scale"], g[f"{tag}_rot"],
+                                            g[f"{tag}_opacity"], g[f"{tag}_sh0"], cam)
+    np.testing.assert_array_equal(pr["valid"], g[f"{tag}_valid"])
+    np.testing.assert_array_equal(pr["bbox"], g[f"{tag}_bbox"])
+    v = g[f"{tag}_valid"]
+    np.testing.assert_allclose(pr["mean2d"][v], g[f"{tag}_mean2d"][v], rtol=1e-12, atol=1e-9)
+    np.testing.assert_allclose(pr["cov2d"][v], g[f"{tag}_cov2d"][v], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(color, g[f"{tag}_color"], atol=1e-12)
+    np.testing.assert_allclose(depth, g[f"{tag}_depth"], atol=1e-11)
+    np.testing.assert_allclose(sil, g[f"{tag}_sil"], atol=1e-12)
