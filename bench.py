@@ -228,6 +228,24 @@ def run_trajectory(args, dev):
             "points_per_scan": float(np.mean([len(f[0]) for f in frames]))}
 
 
+def render_ms(gaussians, cam, reps=10):
+    """Median device time of one 640x480 render of device-resident records
+    (renderer.render_device: projection, depth-ordered tile binning, blend)."""
+    import torch
+    from paper_2410_17084_b200 import renderer as R
+    for _ in range(2):
+        R.render_device(gaussians, cam)
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        R.render_device(gaussians, cam)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
 def run_scans(args):
     """Configs 1 and 3: ms per single scan into an empty map, end to end.
 
@@ -262,7 +280,8 @@ def run_scans(args):
                                  f"into an empty map, H2D + ingest + report D2H",
                      "ms_per_scan": float(np.median(times)), "ms_p90": float(np.percentile(times, 90)),
                      "points": len(pos), "voxels_solved": int(rep.voxels_solved),
-                     "gaussians": int(rep.primitives_added)}
+                     "gaussians": int(rep.primitives_added),
+                     "render_640x480_device_ms": render_ms(eng.gaussians_device(), cam)}
     return out
 
 
@@ -401,6 +420,10 @@ def run_gpu(args, rank, world, local_rank):
                 "traffic": None, "launch_ms": top_ms / top_n, "share_of_step": top_ms / ms}
     stage_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
 
+    # the map's Gaussians (9 per solved voxel) rendered from the bench camera
+    render = {"workload": f"{eng.num_gaussians} Gaussians of the config-4 map, 640x480, "
+                          "renderer.render_device (SURVEY 8(f) row 4)",
+              "device_ms": render_ms(eng.gaussians_device(), cam)}
     traj = None
     if args.traj_scans > 0:
         traj = run_trajectory(args, dev)
@@ -438,6 +461,7 @@ def run_gpu(args, rank, world, local_rank):
             "gpu_launches": launches,
             "trajectory": traj,
             "scans": scans,
+            "render": render,
             "clocks": clk,
             "peaks": {"fp64_tflops_measured": peak64, "hbm_gbs": peaks.get("hbm_gbs")},
         }

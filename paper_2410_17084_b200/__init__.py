@@ -2,7 +2,7 @@
 
 Drop-in for the reference package `voxsplat`'s mapping path
 (`voxel_map`, `gpr`, `splat_init`, plus `PipelineConfig`, `Camera` and the
-error types): same names and signatures, with the arithmetic in hand-written
+error types) and its consumer `renderer`: same names and signatures, with the arithmetic in hand-written
 FP64 sm_100a CUDA kernels behind the C ABI of `include/voxgpr.h`
 (`_lib/libvoxgpr.so`, loaded through `_native`).  There is no CPU path.
 """
@@ -18,6 +18,8 @@ from .gpr import (AxisSelection, GprBatchResult, GprProblem, GprResult, densify_
 from .splat_init import (GaussianMap, GaussianPrimitive, Subgrid, init_color, init_covariance,
                          init_gaussians_batch, init_gaussians_for_voxel, init_position,
                          partition_subgrids)
+from . import renderer
+from .renderer import RenderBuffers, project_points, render
 from .voxel_map import (ColoredPoint, FrameUpdateSet, PointCloud, VoxelCell, VoxelKey, VoxelMap,
                         VoxelPrediction, VoxelState, classify_voxel, update_voxel_variances,
                         voxel_key)
@@ -35,4 +37,5 @@ __all__ = [
     "init_gaussians_batch", "init_gaussians_for_voxel", "init_position", "partition_subgrids",
     "ColoredPoint", "FrameUpdateSet", "PointCloud", "VoxelCell", "VoxelKey", "VoxelMap",
     "VoxelPrediction", "VoxelState", "classify_voxel", "update_voxel_variances", "voxel_key",
+    "renderer", "render", "project_points", "RenderBuffers",
 ]
