@@ -1283,7 +1283,12 @@ __device__ __forceinline__ void dmma_acc(double& c0, double& c1, double a, doubl
 //     (z = L^-1 f, row 0 of tile 0) reduce over the 4 lanes of a row.
 // 11 independent column tiles per voxel at n* = 81.
 template <int NMAX>
-__global__ void __launch_bounds__(128, NMAX <= 16 ? 6 : (NMAX <= 24 ? 4 : 3))
+#ifndef W16_MINB
+#define W16_MINB 6
+#define W24_MINB 4
+#define W32_MINB 3
+#endif
+__global__ void __launch_bounds__(128, NMAX <= 16 ? W16_MINB : (NMAX <= 24 ? W24_MINB : W32_MINB))
 gpr_wdmma_kernel(VoxelSolveArgs va, int mmax, int mm) {
     extern __shared__ __align__(16) double smem[];
     constexpr int LD = NMAX;
