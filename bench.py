@@ -490,8 +490,15 @@ def main():
             if rank != 0:
                 return
         else:
+            # VX_BENCH_BACKEND=gloo: exercise the N>1 code path with several ranks
+            # on one device (a functional check only; numbers need NCCL + N GPUs)
+            backend = os.environ.get("VX_BENCH_BACKEND", "nccl")
+            local_rank %= max(torch.cuda.device_count(), 1)
             torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            else:
+                dist.init_process_group(backend)
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:
