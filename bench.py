@@ -407,7 +407,7 @@ def run_gpu(args, rank, world, local_rank):
                          f"{56 * (float(bucket[top].mean()) + NSTAR):.0f} B/voxel")
         roof = {"kernel": top, "bound": "fp64", "achieved": achieved, "peak": peak64,
                 "unit": "TFLOP/s", "frac": achieved / peak64,
-                "peak_source": "measured in-run DFMA microbenchmark (vx_fp64_peak)",
+                "peak_source": "measured in-run FP64 peak, max of DFMA and DMMA microbenchmarks (vx_fp64_peak)",
                 "traffic": traffic, "traffic_note": tnote, "launch_ms": top_ms / top_n,
                 "share_of_step": top_ms / ms}
     else:

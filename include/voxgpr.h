@@ -335,7 +335,8 @@ int vx_render(const double* d_pos, const double* d_scale, const double* d_rot, c
               double* d_color, double* d_depth, double* d_silhouette, void* stream);
 
 /* ------------------------------------------------------------------------
- * Measurement helper: FP64 FMA peak of this device (DFMA chains, all SMs).
+ * Measurement helper: FP64 peak of this device, max of DFMA chains and
+ * m8n8k4 DMMA chains on all SMs (one shared FP64 datapath).
  * ---------------------------------------------------------------------- */
 int vx_fp64_peak(double* tflops, void* stream);
 
