@@ -211,3 +211,26 @@ def test_monotone_silhouette_bounded_color_and_skip_threshold():
     faint = _splat((0.0, 0.0, 1.0), color=(1, 1, 1), opacity=R.ALPHA_SKIP * 0.5, scale=0.2)
     solid = _splat((0.0, 0.0, 2.0), color=(0, 1, 0), opacity=0.9, scale=0.4)
     np.testing.assert_array_equal(R.render([faint, solid], cam).color, R.render([solid], cam).color)
+
+
+def test_depth_order_needs_low_word():
+    """Depths that share the high 32 bits of their IEEE pattern but arrive out
+    of order (1.0000001 before 1.0): the high-word fast path must fall back to
+    the full 64-bit sort; exact ties keep index order."""
+    cam = _center_camera()
+    a = _splat((0.0, 0.0, 1.0000001), color=(1, 0, 0), opacity=0.6, scale=0.1)
+    b = _splat((0.01, 0.0, 1.0), color=(0, 0, 1), opacity=0.6, scale=0.1)
+    c = _splat((-0.01, 0.0, 1.0), color=(0, 1, 0), opacity=0.6, scale=0.1)   # exact tie with b
+    prims = [a, b, c]
+    buf = R.render(prims, cam)
+    ocam = dict(fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy, width=cam.width, height=cam.height,
+                R=cam.rotation, t=cam.translation)
+    color, depth, sil, _ = O.render_splats(np.stack([p.position for p in prims]),
+                                           np.stack([p.scale for p in prims]),
+                                           np.stack([p.rotation for p in prims]),
+                                           np.array([p.opacity for p in prims]),
+                                           np.stack([p.color for p in prims]), ocam)
+    np.testing.assert_allclose(buf.color, color, atol=1e-13)
+    np.testing.assert_allclose(buf.silhouette, sil, atol=1e-13)
+    # the front splat (b, nearest) dominates the centre pixel colour order
+    assert buf.color[50, 50, 2] > buf.color[50, 50, 0]
