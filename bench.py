@@ -420,6 +420,37 @@ def run_gpu(args, rank, world, local_rank):
                 "traffic": None, "launch_ms": top_ms / top_n, "share_of_step": top_ms / ms}
     stage_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
 
+    # N > 1: the one collective of the path, the hand-off of every rank's
+    # Gaussian records to rank 0 (sharding.gather_records: all-gather of
+    # counts, padded NCCL gather of the SoA fields, stable sort by order key);
+    # reported beside `value`, which stays the data-path throughput
+    gather = None
+    if world > 1 and dist.get_backend() == "nccl":
+        from paper_2410_17084_b200 import sharding
+        recs = eng.gaussians_device()
+        nrec = int(recs["position"].shape[0])
+        order = (torch.arange(nrec, dtype=torch.int64, device=dev) + (int(rank) << 40))
+        for _ in range(2):
+            sharding.gather_records(recs, order, dst=0)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g = sharding.gather_records(recs, order, dst=0)
+        e1.record()
+        torch.cuda.synchronize()
+        gms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        rec_bytes = sum(int(t[0].numel()) * t.element_size() for t in recs.values()) + 8
+        tot = torch.tensor([nrec], dtype=torch.int64, device=dev)
+        dist.all_reduce(tot)
+        gather = {"what": "all ranks' Gaussian records -> rank 0 in global order "
+                          "(sharding.gather_records over NCCL), CUDA events on the "
+                          "current stream, max over ranks",
+                  "records": int(tot.item()), "ms": float(gms.item()),
+                  "bytes_into_rank0": int((int(tot.item()) - nrec) * rec_bytes),
+                  "GB_per_s_into_rank0": (int(tot.item()) - nrec) * rec_bytes / (float(gms.item()) / 1e3) / 1e9}
+        del g
     # the map's Gaussians (9 per solved voxel) rendered from the bench camera
     render = {"workload": f"{eng.num_gaussians} Gaussians of the config-4 map, 640x480, "
                           "renderer.render_device (SURVEY 8(f) row 4)",
@@ -462,6 +493,7 @@ def run_gpu(args, rank, world, local_rank):
             "trajectory": traj,
             "scans": scans,
             "render": render,
+            "gather": gather,
             "clocks": clk,
             "peaks": {"fp64_tflops_measured": peak64, "hbm_gbs": peaks.get("hbm_gbs")},
         }
