@@ -2638,7 +2638,7 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
 #define T64_ROWS 1
 #endif
 #ifndef T96_NRB
-#define T96_NRB 16
+#define T96_NRB 12            // own 96-row instantiation (measured: 6.22 -> 6.07 ms vs the 128-row kernel)
 #define T96_CTW 1
 #define T96_NW 6
 #define T96_MINB 2
