@@ -2693,14 +2693,26 @@ static int launch_big(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_i
     const TileLayout full(n8, mm, MC, m_max, VOXEL, true);
     const int64_t per = use_smem ? int64_t(n8) * PCOLS : full.total;
     int blocks = num_items;
-    int cap = sm_count() * 2;
+    // persistent grid: resident CTAs only (a CTA beyond residency would start
+    // its strided share of the items after a whole resident CTA finished)
+    int per_sm = 2;
+    if (use_smem) {
+        VX_CUDA(cudaFuncSetAttribute(gpr_big_kernel<NW, VOXEL, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gpr_big_kernel<NW, VOXEL, true>,
+                                                              NW * 32, smem));
+    } else {
+        VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gpr_big_kernel<NW, VOXEL, false>,
+                                                              NW * 32, 0));
+    }
+    if (per_sm < 1) per_sm = 1;
+    int cap = sm_count() * per_sm;
     const int64_t max_blocks = (int64_t(4) << 30) / (per * 8);
     if (cap > max_blocks) cap = int(max_blocks > 0 ? max_blocks : 1);
     if (blocks > cap) blocks = cap;
     VX_TRY(work.reserve(size_t(per) * 8 * blocks, s));
     if (use_smem) {
         auto kfn = gpr_big_kernel<NW, VOXEL, true>;
-        VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         kfn<<<blocks, NW * 32, smem, s>>>(va, pa, m_max, mm, n_max, work.as<double>(), per);
     } else {
         gpr_big_kernel<NW, VOXEL, false><<<blocks, NW * 32, 0, s>>>(va, pa, m_max, mm, n_max,
