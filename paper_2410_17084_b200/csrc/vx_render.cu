@@ -23,6 +23,7 @@
 // value differs from the reference only through exp() (<= 1 ulp) and the
 // covariance's 3x3 products (einsum order).
 #include <cmath>
+#include <mutex>
 
 #include "vx_common.cuh"
 #include "vx_internal.h"
@@ -293,7 +294,8 @@ struct RenderScratch {
     DevBuf mean2d, cov2d, depth, radius, valid, bbox, ntiles, flags, scan, klo, khi, idx, klo2, khi2,
         idx2, order, cnt, off, tkey, tval, tkey2, tval2, tstart, tend, tmp, sort_tmp;
 };
-RenderScratch g_rs;
+RenderScratch g_rs;          // process-wide scratch, grown on demand
+std::mutex g_rs_mu;          // one render at a time per process (host threads)
 }  // namespace
 
 int launch_project(const double* pos, const double* scale, const double* rot, int64_t n,
@@ -318,6 +320,7 @@ int render_splats(const double* pos, const double* scale, const double* rot, con
     const int W = cam.width, H = cam.height;
     const int tiles_x = (W + RT - 1) / RT, tiles_y = (H + RT - 1) / RT;
     const int ntl = tiles_x * tiles_y;
+    std::lock_guard<std::mutex> lk(g_rs_mu);
     RenderScratch& r = g_rs;
     if (n >= (int64_t(1) << 31) - 1) {
         set_error("render: %lld primitives exceed the 2^31 limit", (long long)n);
