@@ -296,6 +296,8 @@ struct RenderScratch {
 };
 RenderScratch g_rs;          // process-wide scratch, grown on demand
 std::mutex g_rs_mu;          // one render at a time per process (host threads)
+cudaEvent_t g_rs_done = nullptr;   // last render's kernels: a render on another
+                                   // stream waits for them before reusing scratch
 }  // namespace
 
 int launch_project(const double* pos, const double* scale, const double* rot, int64_t n,
@@ -314,13 +316,29 @@ int project_points(const double* pos, const double* scale, const double* rot, in
     return launch_project(pos, scale, rot, n, cam, near, o, s);
 }
 
+static int render_splats_impl(const double* pos, const double* scale, const double* rot,
+                              const double* opacity, const double* sh0, int64_t n,
+                              const VxCamera& cam, double near, double* color, double* depth,
+                              double* sil, cudaStream_t s);
+
 int render_splats(const double* pos, const double* scale, const double* rot, const double* opacity,
                   const double* sh0, int64_t n, const VxCamera& cam, double near, double* color,
                   double* depth, double* sil, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_rs_mu);
+    if (g_rs_done == nullptr) VX_CUDA(cudaEventCreateWithFlags(&g_rs_done, cudaEventDisableTiming));
+    VX_CUDA(cudaStreamWaitEvent(s, g_rs_done, 0));
+    const int rc = render_splats_impl(pos, scale, rot, opacity, sh0, n, cam, near, color, depth, sil, s);
+    VX_CUDA(cudaEventRecord(g_rs_done, s));
+    return rc;
+}
+
+static int render_splats_impl(const double* pos, const double* scale, const double* rot,
+                              const double* opacity, const double* sh0, int64_t n,
+                              const VxCamera& cam, double near, double* color, double* depth,
+                              double* sil, cudaStream_t s) {
     const int W = cam.width, H = cam.height;
     const int tiles_x = (W + RT - 1) / RT, tiles_y = (H + RT - 1) / RT;
     const int ntl = tiles_x * tiles_y;
-    std::lock_guard<std::mutex> lk(g_rs_mu);
     RenderScratch& r = g_rs;
     if (n >= (int64_t(1) << 31) - 1) {
         set_error("render: %lld primitives exceed the 2^31 limit", (long long)n);
