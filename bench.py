@@ -419,6 +419,24 @@ def run_gpu(args, rank, world, local_rank):
                 "frac": achieved / pk, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "traffic": None, "launch_ms": top_ms / top_n, "share_of_step": top_ms / ms}
     stage_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
+    # every stage against its own roof (north star: HBM GB/s for hashing and
+    # Gaussian init, FP64 for the solves); algorithmic work per SURVEY 8(d)
+    hbm = float(peaks.get("hbm_gbs", 6548.8))
+    stage_roofline = {}
+    for k, (tms, _) in prof.items():
+        if tms <= 0 or k in ("densify",):
+            continue
+        if k in bucket and len(bucket[k]):
+            tf = float(gpr_flops(bucket[k]).sum()) * args.steps / (tms / 1e3) / 1e12
+            stage_roofline[k] = {"bound": "fp64", "achieved": round(tf, 3), "unit": "TFLOP/s",
+                                 "frac": round(tf / peak64, 4), "voxels": int(len(bucket[k]))}
+        elif k in ("hash", "splat", "pca"):
+            per = {"hash": 104.0 * npts,                    # read xyz+rgb, write xyz, rgb, noise
+                   "splat": (81 * 56 + 9 * 136) * float(solved_expected),
+                   "pca": 24.0 * float(counts[counts >= TAU].sum())}[k]
+            gbs = per * args.steps / (tms / 1e3) / 1e9
+            stage_roofline[k] = {"bound": "hbm", "achieved": round(gbs, 1), "unit": "GB/s",
+                                 "frac": round(gbs / hbm, 4)}
 
     # N > 1: the one collective of the path, the hand-off of every rank's
     # Gaussian records to rank 0 (sharding.gather_records: all-gather of
@@ -483,6 +501,7 @@ def run_gpu(args, rank, world, local_rank):
                        "parallelism": f"hash-shard x{world}"},
             "roofline": roof,
             "stage_ms": stage_ms,
+            "stage_roofline": stage_roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
