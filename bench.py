@@ -14,10 +14,18 @@ map (weak scaling, no data-path collective: the path shards by voxel).
 
 `value` is timed with CUDA events on the launching stream with inputs already
 in HBM; `e2e` runs the same step through the public API
-(`MappingEngine.ingest`) from pinned host tensors (H2D of points, colours
-and image inside the timed region, D2H of the ingest report).  `--impl
-reference` times the CPU oracle (NumPy/SciPy restatement of the reference,
-oracle/voxsplat_oracle.py) on a bounded sample with all host cores.
+(`MappingEngine.ingest_stream`) from pinned host tensors (H2D of points,
+colours and image inside the timed region, D2H of the ingest report).
+`--impl reference` times the CPU oracle (NumPy/SciPy restatement of the
+reference, oracle/voxsplat_oracle.py) on a bounded sample with all host cores.
+
+Extra keys on the JSON line: `roofline` (dominant kernel vs the in-run FP64
+peak, DRAM traffic from the committed ncu capture), `stage_roofline` (every
+stage vs its roof), `stage_ms`, `trajectory` (config 2, ms/scan with
+re-fits), `scans` (configs 1 and 3, ms per single scan through the host API,
+plus a 640x480 render of the scan's Gaussians), `render` (the config-4 map's
+Gaussians rendered at 640x480), `gather` (N > 1: NCCL hand-off of every
+rank's Gaussian records to rank 0), `cpu_baseline`, `clocks`, `gpu_launches`.
 """
 
 from __future__ import annotations
