@@ -113,3 +113,24 @@ def test_config_roundtrip():
     c = vx.PipelineConfig.from_mapping({"voxel_size": "0.5", "tau": "12", "kernel": "matern52"})
     assert c.voxel_size == 0.5 and c.tau == 12 and c.kernel == "matern52"
     assert any(line.startswith("voxel_size=") for line in c.to_lines())
+
+
+def test_renderer_host_helpers_match_reference_semantics():
+    """renderer.py host helpers (the reference exposes them, renderer.py:150-179):
+    depth_order is stable with index ties; alpha_patch applies ceiling and skip;
+    render() itself has no CPU path."""
+    from paper_2410_17084_b200 import renderer as R
+    depth = np.array([2.0, 1.0, 1.0, 3.0, 0.5])
+    valid = np.array([True, True, True, False, True])
+    np.testing.assert_array_equal(R.depth_order(depth, valid), [4, 1, 2, 0])
+    a = R.alpha_patch(np.array([1.0, 1.0]), np.array([[0.5, 0.0], [0.0, 0.5]]), 1.0, 0, 3, 0, 3)
+    assert a.max() == R.ALPHA_CEILING                       # centre clamped to 0.99
+    faint = R.alpha_patch(np.array([1.0, 1.0]), np.eye(2), 0.5 / 255.0, 0, 3, 0, 3)
+    assert np.all(faint == 0.0)                             # below 1/255: skipped
+    g = R.gaussian_patch(np.array([0.0, 0.0]), np.eye(2), 0, 2, 0, 1)
+    np.testing.assert_allclose(g, [[1.0, np.exp(-0.5)]])
+    import torch
+    if not torch.cuda.is_available():
+        from paper_2410_17084_b200 import _native as N
+        with pytest.raises(N.NativeUnavailable):
+            R.render([], vx.Camera(fx=1, fy=1, cx=0, cy=0, width=4, height=4))
