@@ -103,7 +103,7 @@ def test_error_isolation_and_jitter_rule():
     assert vx.gpr_solve_batch([bad]).ok == oracle_ok
 
 
-@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 64, 65, 100, 200, 400])
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 64, 65, 100, 150, 200, 400])
 def test_size_buckets_against_oracle(n):
     """Every kernel bucket (team n<=32, team n<=64, generic) against the oracle.
 
