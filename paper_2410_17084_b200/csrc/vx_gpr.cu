@@ -29,6 +29,7 @@
 // Both write the prediction (points, colours, clipped variances) into the
 // voxel's prediction slot — which is also the pseudo-observation set of its
 // next solve — and update the lifecycle state in the same kernel.
+#include <atomic>
 #include <cfloat>
 #include <cstdlib>
 #include <cmath>
@@ -1987,9 +1988,22 @@ __device__ void team_voxel_epilogue(const VoxelSolveArgs& va, const VoxelCtx& c,
     }
 }
 
+// Dynamic item queue of the persistent tile grids: a CTA's first item is
+// blockIdx.x, later ones come from an atomic counter, so CTAs that drew small
+// voxels take more of them (measured: the tile buckets 18.6 -> 18.2 ms vs the
+// static blockIdx + k * gridDim stride).  Each launch takes its own counter
+// from a ring, so launches on concurrent streams never share one.
+constexpr int TILE_CTR_RING = 1024;
+__device__ int g_tile_ctr[TILE_CTR_RING];
+__device__ __forceinline__ int tile_next(int* s_next, int* ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) *s_next = int(gridDim.x) + atomicAdd(ctr, 1);
+    __syncthreads();
+    return *s_next;
+}
 template <int NRB, int CTW, int NW, int MINB, int ROWS, bool VOXEL>
 __global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs va, ProblemArgs pa,
-                                                           int mmax, int mm) {
+                                                           int mmax, int mm, int* ctr) {
     extern __shared__ __align__(16) double smem[];
     constexpr int N8 = NRB * 8;
     constexpr int NT = NW * 32;
@@ -2015,7 +2029,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) gpr_tile_kernel(VoxelSolveArgs 
         __syncthreads();
     }
 
-    for (int it = blockIdx.x; it < num_items; it += gridDim.x) {
+    __shared__ int s_next;
+    for (int it = blockIdx.x; it < num_items; it = tile_next(&s_next, ctr)) {
 #ifdef VX_PHASE_TIMING
         long long tph = clock64();
 #endif
@@ -2677,7 +2692,12 @@ static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     int blocks = num_items;
     const int cap = sm_count() * per_sm;
     if (blocks > cap) blocks = cap;
-    kfn<<<blocks, NW * 32, smem, s>>>(va, pa, m_max, mm);
+    static std::atomic<unsigned> ring{0};
+    int* ctr = nullptr;
+    VX_CUDA(cudaGetSymbolAddress(reinterpret_cast<void**>(&ctr), g_tile_ctr));
+    ctr += ring.fetch_add(1) % TILE_CTR_RING;
+    VX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), s));
+    kfn<<<blocks, NW * 32, smem, s>>>(va, pa, m_max, mm, ctr);
     count_launch();
     VX_CHECK_LAUNCH();
     return VX_OK;
