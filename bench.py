@@ -2,30 +2,35 @@
 """Benchmark: per-voxel GPR + Gaussian-init throughput (voxels/s, ms/scan).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--voxels V] [--workload map|scan]
+                    [--voxels V]
 
-Default workload (BASELINE.json config 4 on one GPU): a ~1M-voxel synthetic
-planar map (points-per-voxel histogram of the 32-beam scan, ~25.5M points,
-0.5 m voxels) ingested as ONE scan into an empty map: hash -> per-voxel
-FP64 GPR (81-point grid) -> Gaussian init for every first solve.  A step is
-one such ingest into a freshly cleared map.  Inputs (1.2 GB) exceed L2, so
-no explicit flush is needed.  Under torchrun each rank ingests its own 1M-voxel
-map (weak scaling, no data-path collective: the path shards by voxel).
+Default workload (BASELINE.json config 4): ONE ~1M-voxel synthetic planar map
+(points-per-voxel histogram of the 32-beam scan, ~25.5M points, 0.5 m voxels)
+ingested as ONE scan into an empty map: hash -> per-voxel FP64 GPR (81-point
+grid) -> Gaussian init for every first solve.  A step is one such ingest into
+a freshly cleared map.  Inputs (1.2 GB) exceed L2, so no explicit flush is
+needed.  Under torchrun the same map is hash-sharded over the ranks
+(`ShardedEngine`: every rank holds the whole scan, keeps the voxels it owns;
+strong scaling, no data-path collective), and the frame's predictions and
+Gaussian records are gathered to rank 0 over NCCL (`gather`, and inside `e2e`).
 
 `value` is timed with CUDA events on the launching stream with inputs already
-in HBM; `e2e` runs the same step through the public API
-(`MappingEngine.ingest_stream`) from pinned host tensors (H2D of points,
-colours and image inside the timed region, D2H of the ingest report).
-`--impl reference` times the CPU oracle (NumPy/SciPy restatement of the
-reference, oracle/voxsplat_oracle.py) on a bounded sample with all host cores.
+in HBM, max over ranks; `e2e` runs the same step through the public API
+(`MappingEngine.ingest_stream(fetch_records=True)`) from pinned host tensors:
+H2D of points, colours and image, and D2H of the frame's Gaussian records into
+pinned host memory, both inside the timed region (`e2e_map_resident`: the
+round-1 variant without the record D2H).  `--impl reference` times the CPU
+oracle (NumPy/SciPy restatement of the reference, oracle/voxsplat_oracle.py)
+on a bounded sample with all host cores; `cpu_baseline` is the same
+measurement in a fresh subprocess.
 
 Extra keys on the JSON line: `roofline` (dominant kernel vs the in-run FP64
 peak, DRAM traffic from the committed ncu capture), `stage_roofline` (every
-stage vs its roof), `stage_ms`, `trajectory` (config 2, ms/scan with
-re-fits), `scans` (configs 1 and 3, ms per single scan through the host API,
-plus a 640x480 render of the scan's Gaussians), `render` (the config-4 map's
-Gaussians rendered at 640x480), `gather` (N > 1: NCCL hand-off of every
-rank's Gaussian records to rank 0), `cpu_baseline`, `clocks`, `gpu_launches`.
+stage vs its roof), `stage_ms`, `tail` (config 4 with the Livox n-histogram),
+`trajectory` (config 2, ms/scan with re-fits), `scans` (configs 1 and 3, ms
+per single scan through the host API, plus a 640x480 render of the scan's
+Gaussians), `render` (the config-4 map's Gaussians rendered at 640x480),
+`gather` (N > 1), `cpu_baseline`, `clocks`, `gpu_launches`.
 """
 
 from __future__ import annotations
@@ -139,6 +144,13 @@ class Clocks:
 # CPU oracle leg (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
 
+_JOBS = []   # set before the worker pool forks: workers inherit, nothing is pickled
+
+
+def _oracle_job(i):
+    return _oracle_worker(_JOBS[i])
+
+
 def _oracle_worker(args):
     pos, col, cam, img, cfg = args
     from oracle import voxsplat_oracle as O
@@ -150,53 +162,181 @@ def _oracle_worker(args):
     return len(res["predictions"]), time.perf_counter() - t0
 
 
-def cpu_oracle_rate(pos, col, owner, cam, img, sample_every, procs):
-    """Oracle ingest of every `sample_every`-th voxel, split over `procs` processes."""
-    mask = owner % sample_every == 0
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_line(args, world):
+    """The CPU oracle on a bounded sample of the config-4 map, all host cores.
+
+    A step = the oracle's store_frame -> densify -> Gaussian init of every
+    `ref_sample`-th voxel of the map, split over P single-BLAS-thread worker
+    processes (pool started before the timed steps); `ms_per_step` is that
+    measured sample step, the full-map time is extrapolated in its own field.
+    """
+    procs = len(os.sched_getaffinity(0))
+    pos, col, counts, keys, owner, cam, img = make_workload(args.voxels, 0)
+    mask = owner % args.ref_sample == 0
     spos, scol, sown = pos[mask], col[mask], owner[mask]
-    shard = (sown // sample_every) % procs
-    jobs = [(spos[shard == r], scol[shard == r], cam, img, None) for r in range(procs)]
-    t0 = time.perf_counter()
-    if procs > 1:
-        with mp.get_context("fork").Pool(procs) as pool:
-            out = pool.map(_oracle_worker, jobs)
-    else:
-        out = [_oracle_worker(j) for j in jobs]
-    wall = time.perf_counter() - t0
-    solved = sum(o[0] for o in out)
-    return solved / wall, solved, wall, int(mask.sum())
+    shard = (sown // args.ref_sample) % procs
+    _JOBS[:] = [(spos[shard == r], scol[shard == r], cam, img, None) for r in range(procs)]
+    walls, rates, busy = [], [], []
+    with mp.get_context("fork").Pool(procs) as pool:
+        pool.map(_noop, range(procs))                 # workers up before timing
+        # (no warm-up steps: the oracle keeps no state between steps)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            out = pool.map(_oracle_job, range(procs), chunksize=1)
+            wall = time.perf_counter() - t0
+            solved = sum(o[0] for o in out)
+            walls.append(wall)
+            rates.append(solved / wall)
+            busy.append(max(o[1] for o in out))
+    v = float(np.median(rates))
+    ms = float(np.median(walls)) * 1e3
+    full = args.voxels * (counts >= TAU).mean()
+    sample = (f"every {args.ref_sample}th voxel of the {args.voxels}-voxel map ({solved} solved "
+              f"voxels, {int(mask.sum())} points) per step, {procs} worker processes "
+              f"(1 BLAS thread each), {cpu_model()}")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "ms_per_step_what": "measured wall time of one sample step (the bounded sample below)",
+            "ms_full_map_extrapolated": full / v * 1e3,
+            "slowest_worker_ms": float(np.median(busy)) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config4: ONE {args.voxels}-voxel planar map, one scan, "
+                                   "0.5 m voxels (bounded sample)", "voxels": args.voxels},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
+                             "sample": sample, "cpu_model": cpu_model()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _noop(_):
+    return 0
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    procs = len(os.sched_getaffinity(0))
-    pos, col, counts, keys, owner, cam, img = make_workload(args.voxels, 0)
-    rates = []
-    for _ in range(args.warmup):
-        pass   # the oracle has no warm-up state; W is honoured by not timing anything
-    for _ in range(args.steps):
-        r, solved, wall, npts = cpu_oracle_rate(pos, col, owner, cam, img, args.ref_sample, procs)
-        rates.append(r)
-    v = float(np.median(rates))
-    ms = args.voxels * (counts >= TAU).mean() / v * 1e3
-    sample = (f"every {args.ref_sample}th voxel of the {args.voxels}-voxel map "
-              f"({solved} solved voxels, {npts} points) per step, {procs} processes")
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": f"config4: {args.voxels}-voxel planar map, one scan, 0.5 m voxels",
-                       "voxels": args.voxels},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(reference_line(args, world)), flush=True)
+
+
+def cpu_baseline_subprocess(args):
+    """cpu_baseline of the GPU line: the SAME measurement as `--impl reference`,
+    run in a fresh process (no CUDA context, nothing forked from this one)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+           "--warmup", "0", "--voxels", str(args.voxels), "--ref-sample", str(args.ref_sample)]
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+        line = json.loads(out.stdout.strip().splitlines()[-1])
+        cb = dict(line["cpu_baseline"])
+        cb["sample_ms"] = line["ms_per_step"]
+        return cb
+    except Exception as e:   # reported, never fatal for the GPU line
+        return {"value": None, "unit": UNIT, "error": f"{type(e).__name__}: {e}"}
 
 
 # ---------------------------------------------------------------------------
 # GPU leg
 # ---------------------------------------------------------------------------
+
+def buckets_of(sol):
+    """Training-set sizes of the solved voxels per size bucket (csrc launch_voxel_solve)."""
+    return {"gpr_n16": sol[sol <= 16], "gpr_n24": sol[(sol > 16) & (sol <= 24)],
+            "gpr_n32": sol[(sol > 24) & (sol <= 32)],
+            "gpr_n64": sol[(sol > 32) & (sol <= 64)],
+            "gpr_n96": sol[(sol > 64) & (sol <= 96)],
+            "gpr_n128": sol[(sol > 96) & (sol <= 128)],
+            "gpr_n160": sol[(sol > 128) & (sol <= 160)], "gpr_n_large": sol[sol > 160]}
+
+
+def stage_report(prof, counts, npts, steps, peak64, hbm):
+    """(stage_ms, stage_roofline): every stage against its own roof (north star:
+    HBM GB/s for hashing and Gaussian init, FP64 for the solves); algorithmic
+    work per SURVEY 8(d)."""
+    sol = counts[counts >= TAU]
+    bucket = buckets_of(sol)
+    stage_ms = {k: round(v[0] / steps, 4) for k, v in prof.items()}
+    stage_roofline = {}
+    for k, (tms, _) in prof.items():
+        if tms <= 0 or k in ("densify",):
+            continue
+        if k in bucket and len(bucket[k]):
+            tf = float(gpr_flops(bucket[k]).sum()) * steps / (tms / 1e3) / 1e12
+            stage_roofline[k] = {"bound": "fp64", "achieved": round(tf, 3), "unit": "TFLOP/s",
+                                 "frac": round(tf / peak64, 4), "voxels": int(len(bucket[k]))}
+        elif k in ("hash", "splat", "pca"):
+            per = {"hash": 104.0 * npts,                    # read xyz+rgb, write xyz, rgb, noise
+                   "splat": (81 * 56 + 9 * 136) * float(len(sol)),
+                   "pca": 24.0 * float(sol.sum())}[k]
+            gbs = per * steps / (tms / 1e3) / 1e9
+            stage_roofline[k] = {"bound": "hbm", "achieved": round(gbs, 1), "unit": "GB/s",
+                                 "frac": round(gbs / hbm, 4)}
+    return stage_ms, stage_roofline
+
+
+def run_tail(args, peak64, hbm):
+    """Config 4, tail variant: the same 1M-voxel planar map with
+    the points-per-voxel histogram of the Livox-style rosette scan (config 3,
+    n up to ~750), ingested as one scan; device-timed with inputs in HBM."""
+    import torch
+    import paper_2410_17084_b200 as vx
+    from paper_2410_17084_b200 import _native as N
+    pos, col, counts, keys, owner = scenes.planar_map(args.tail_voxels, voxel_size=0.5, seed=5,
+                                                      bins=scenes.TAIL_BINS, probs=scenes.TAIL_PROBS)
+    side = int(math.ceil(math.sqrt(args.tail_voxels)))
+    R, t = scenes.look_at((0.25 * side, 0.25 * side, 150.0), (0.25 * side, 0.25 * side + 1e-3, 0.0),
+                          up=(0.0, 1.0, 0.0))
+    cam = vx.Camera(500.0, 500.0, 319.5, 239.5, 640, 480, R, t)
+    img = torch.from_numpy(np.random.default_rng(98).uniform(0.0, 1.0, (480, 640, 3))).cuda()
+    npts = len(pos)
+    d_xyz, d_rgb = torch.from_numpy(pos).cuda(), torch.from_numpy(col).cuda()
+    solved = int((counts >= TAU).sum())
+    eng = vx.MappingEngine(vx.PipelineConfig(voxel_size=0.5, tau=TAU),
+                           voxel_capacity=int(args.tail_voxels * 1.05), point_capacity=int(npts * 1.6),
+                           gaussian_capacity=9 * solved + 1024)
+    steps = max(1, min(args.steps, args.tail_steps))
+    for _ in range(2):
+        eng.reset()
+        rep = eng.ingest_device(d_xyz, d_rgb, npts, cam, img)
+    torch.cuda.synchronize()
+    N.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        eng.reset()
+        rep = eng.ingest_device(d_xyz, d_rgb, npts, cam, img)
+    e1.record()
+    torch.cuda.synchronize()
+    prof = N.profile_read()
+    N.profile(False)
+    ms = e0.elapsed_time(e1) / steps
+    stage_ms, stage_roof = stage_report(prof, counts, npts, steps, peak64, hbm)
+    sol = counts[counts >= TAU]
+    flops = float(gpr_flops(sol).sum())
+    gpr_ms = sum(v for k, v in stage_ms.items() if k.startswith("gpr_"))
+    out = {"workload": f"config4 tail variant: {args.tail_voxels}-voxel planar map, config-3 "
+                       f"(Livox rosette) points-per-voxel histogram, n {int(sol.min())}-{int(sol.max())}, "
+                       f"{npts} points, one scan",
+           "steps": steps, "ms_per_step": ms, "voxels_per_s": rep.voxels_solved / (ms / 1e3),
+           "voxels_solved": int(rep.voxels_solved), "expected_solved": solved,
+           "gpr_fp64_tflops": flops / (gpr_ms / 1e3) / 1e12 if gpr_ms else None,
+           "gpr_frac_of_fp64_peak": flops / (gpr_ms / 1e3) / 1e12 / peak64 if gpr_ms else None,
+           "stage_ms": stage_ms, "stage_roofline": stage_roof,
+           "n_hist": {k: int(len(v)) for k, v in buckets_of(sol).items()}}
+    del eng, d_xyz, d_rgb
+    torch.cuda.empty_cache()
+    return out
+
 
 def run_trajectory(args, dev):
     """Config 2: a trajectory of 32-beam scans (pose +1 m/scan) with GPR re-fits.
@@ -316,26 +456,58 @@ def run_gpu(args, rank, world, local_rank):
     h_rgb = torch.from_numpy(col).pin_memory()
     h_img = torch.from_numpy(img).pin_memory()
     d_xyz, d_rgb, d_img = (t.to(dev) for t in (h_xyz, h_rgb, h_img))
-    eng = vx.MappingEngine(config, voxel_capacity=int(args.voxels * 1.05),
-                           point_capacity=int(npts * 1.6),
-                           gaussian_capacity=9 * solved_expected + 1024)
+    sharded = None
+    if world > 1:
+        # ONE config-4 map hash-sharded over the ranks: every rank
+        # holds the whole scan, its hashing kernel keeps the keys it owns
+        from paper_2410_17084_b200 import sharding
+        sharded = sharding.ShardedEngine(config, rank, world,
+                                         voxel_capacity=int(args.voxels * 1.05 / world) + 4096,
+                                         point_capacity=int(npts * 1.6 / world) + 65536,
+                                         gaussian_capacity=9 * solved_expected // world + 65536)
+        eng = sharded.engine
+    else:
+        eng = vx.MappingEngine(config, voxel_capacity=int(args.voxels * 1.05),
+                               point_capacity=int(npts * 1.6),
+                               gaussian_capacity=9 * solved_expected + 1024)
 
     def step_device():
         eng.reset()
         return eng.ingest_device(d_xyz, d_rgb, npts, cam, d_img)
 
+    fetched = {"records": 0, "bytes": 0}
+
+    def got_records(rep, host):
+        # the frame's Gaussian records have landed in pinned host memory
+        fetched["records"] = int(host["position"].shape[0]) if host else 0
+        fetched["bytes"] = sum(int(t.numel()) * t.element_size() for t in host.values())
+
     def run_e2e(k):
         # public streaming API: pinned host frames, H2D of frame i+1 overlapped
-        # with the device work of frame i; ingest reports read back every frame
+        # with the device work of frame i; each frame's Gaussian records D2H into
+        # pinned host memory overlapped with frame i+1 (the host GaussianMap of
+        # pipeline.py:161-171); N > 1: the frame's predictions + records are also
+        # gathered to rank 0 over NCCL (sharding.gather_frame)
+        frames = [(h_xyz, h_rgb, cam, h_img)] * k
+        on_frame = (lambda rep: sharded.gather_frame(dst=0)) if sharded is not None else None
+        return eng.ingest_stream(frames, reset_each=True, on_frame=on_frame,
+                                 fetch_records=True, on_records=got_records)
+
+    def run_e2e_resident(k):
+        # variant kept for comparison with round 1: outputs stay in HBM
         frames = [(h_xyz, h_rgb, cam, h_img)] * k
         return eng.ingest_stream(frames, reset_each=True)
 
     for _ in range(args.warmup):
         rep = step_device()
-    run_e2e(2)            # warm the streaming path (side stream + double buffers)
+    run_e2e(3)            # warm the streaming path (side streams + double buffers)
+    run_e2e_resident(2)
     torch.cuda.synchronize()
-    if rep.voxels_solved < 0.99 * solved_expected:
-        raise RuntimeError(f"solved {rep.voxels_solved} of {solved_expected} expected voxels")
+    chk = torch.tensor([float(rep.voxels_solved)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(chk)
+    if chk.item() < 0.99 * solved_expected:
+        raise RuntimeError(f"solved {chk.item()} of {solved_expected} expected voxels")
     peak64 = N.fp64_peak_tflops()
     peaks = {}
     try:
@@ -383,20 +555,17 @@ def run_gpu(args, rank, world, local_rank):
     e2e_ms, e2e_reps, _, _ = timed(lambda: run_e2e(args.steps), 1)
     e2e_wall_ms = (time.perf_counter() - t_wall) * 1e3
     e2e_value = float(tot_solved.item()) / (e2e_ms / args.steps / 1e3)
+    res_ms, _, _, _ = timed(lambda: run_e2e_resident(args.steps), 1)
     h2d = h_xyz.numel() * 8 + h_rgb.numel() * 8 + h_img.numel() * 8
-    d2h = 7 * 8 * 2 + 21 * 8   # frame/densify info structs + counters per step
+    # Gaussian records of the frame (136 B each) + frame/densify info structs
+    d2h = fetched["bytes"] + 7 * 8 * 2 + 21 * 8
 
     # roofline of the dominant kernel (FP64 pipe for the GPR solves)
     stages = {k: v for k, v in prof.items() if k != "densify" and v[1] > 0}
     top = max(stages, key=lambda k: stages[k][0])
     top_ms, top_n = stages[top]
     sol = counts[counts >= TAU]
-    bucket = {"gpr_n16": sol[sol <= 16], "gpr_n24": sol[(sol > 16) & (sol <= 24)],
-              "gpr_n32": sol[(sol > 24) & (sol <= 32)],
-              "gpr_n64": sol[(sol > 32) & (sol <= 64)],
-              "gpr_n96": sol[(sol > 64) & (sol <= 96)],
-              "gpr_n128": sol[(sol > 96) & (sol <= 128)],
-              "gpr_n160": sol[(sol > 128) & (sol <= 160)], "gpr_n_large": sol[sol > 160]}
+    bucket = buckets_of(sol)
     if top in bucket:
         flops = float(gpr_flops(bucket[top]).sum()) * args.steps
         achieved = flops / (top_ms / 1e3) / 1e12
@@ -426,61 +595,43 @@ def run_gpu(args, rank, world, local_rank):
         roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s",
                 "frac": achieved / pk, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "traffic": None, "launch_ms": top_ms / top_n, "share_of_step": top_ms / ms}
-    stage_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
-    # every stage against its own roof (north star: HBM GB/s for hashing and
-    # Gaussian init, FP64 for the solves); algorithmic work per SURVEY 8(d)
     hbm = float(peaks.get("hbm_gbs", 6548.8))
-    stage_roofline = {}
-    for k, (tms, _) in prof.items():
-        if tms <= 0 or k in ("densify",):
-            continue
-        if k in bucket and len(bucket[k]):
-            tf = float(gpr_flops(bucket[k]).sum()) * args.steps / (tms / 1e3) / 1e12
-            stage_roofline[k] = {"bound": "fp64", "achieved": round(tf, 3), "unit": "TFLOP/s",
-                                 "frac": round(tf / peak64, 4), "voxels": int(len(bucket[k]))}
-        elif k in ("hash", "splat", "pca"):
-            per = {"hash": 104.0 * npts,                    # read xyz+rgb, write xyz, rgb, noise
-                   "splat": (81 * 56 + 9 * 136) * float(solved_expected),
-                   "pca": 24.0 * float(counts[counts >= TAU].sum())}[k]
-            gbs = per * args.steps / (tms / 1e3) / 1e9
-            stage_roofline[k] = {"bound": "hbm", "achieved": round(gbs, 1), "unit": "GB/s",
-                                 "frac": round(gbs / hbm, 4)}
+    stage_ms, stage_roofline = stage_report(prof, counts, npts, args.steps, peak64, hbm)
 
-    # N > 1: the one collective of the path, the hand-off of every rank's
-    # Gaussian records to rank 0 (sharding.gather_records: all-gather of
-    # counts, padded NCCL gather of the SoA fields, stable sort by order key);
-    # reported beside `value`, which stays the data-path throughput
+    # N > 1: the one collective of the path, the hand-off of the
+    # frame's predictions and Gaussian records from every shard to rank 0
+    # (sharding.gather_frame: all-gather of counts, grouped NCCL send/recv
+    # gather-v, stable sort by the first-touch order key); timed after a step
     gather = None
-    if world > 1 and dist.get_backend() == "nccl":
-        from paper_2410_17084_b200 import sharding
-        recs = eng.gaussians_device()
-        nrec = int(recs["position"].shape[0])
-        order = (torch.arange(nrec, dtype=torch.int64, device=dev) + (int(rank) << 40))
+    if sharded is not None:
+        step_device()
         for _ in range(2):
-            sharding.gather_records(recs, order, dst=0)
+            sharded.gather_frame(dst=0)
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        g = sharding.gather_records(recs, order, dst=0)
+        g = sharded.gather_frame(dst=0)
         e1.record()
         torch.cuda.synchronize()
         gms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         dist.all_reduce(gms, op=dist.ReduceOp.MAX)
-        rec_bytes = sum(int(t[0].numel()) * t.element_size() for t in recs.values()) + 8
-        tot = torch.tensor([nrec], dtype=torch.int64, device=dev)
-        dist.all_reduce(tot)
-        gather = {"what": "all ranks' Gaussian records -> rank 0 in global order "
-                          "(sharding.gather_records over NCCL), CUDA events on the "
-                          "current stream, max over ranks",
-                  "records": int(tot.item()), "ms": float(gms.item()),
-                  "bytes_into_rank0": int((int(tot.item()) - nrec) * rec_bytes),
-                  "GB_per_s_into_rank0": (int(tot.item()) - nrec) * rec_bytes / (float(gms.item()) / 1e3) / 1e9}
+        if rank == 0:
+            nb = sum(int(v.numel()) * v.element_size() for part in g.values() for v in part.values())
+            gather = {"what": "frame predictions (81 x xyz, rgb, var) + Gaussian records of every "
+                              "shard -> rank 0 in global first-touch order (sharding.gather_frame: "
+                              "grouped NCCL send/recv gather-v + order-key sort), CUDA events, "
+                              "max over ranks",
+                      "voxels": int(g["predictions"]["keys"].shape[0]),
+                      "records": int(g["gaussians"]["position"].shape[0]),
+                      "ms": float(gms.item()), "bytes_at_rank0": nb,
+                      "GB_per_s_into_rank0": nb * (world - 1) / world / (float(gms.item()) / 1e3) / 1e9}
         del g
     # the map's Gaussians (9 per solved voxel) rendered from the bench camera
     render = {"workload": f"{eng.num_gaussians} Gaussians of the config-4 map, 640x480, "
                           "renderer.render_device (SURVEY 8(f) row 4)",
               "device_ms": render_ms(eng.gaussians_device(), cam)}
+    tail = run_tail(args, peak64, hbm) if (args.tail_voxels > 0 and world == 1) else None
     traj = None
     if args.traj_scans > 0:
         traj = run_trajectory(args, dev)
@@ -488,25 +639,23 @@ def run_gpu(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        procs = len(os.sched_getaffinity(0))
-        r, s_solved, wall, spts = cpu_oracle_rate(pos, col, owner, cam_d, img, args.ref_sample,
-                                                  procs)
-        cpu = {"value": r, "unit": UNIT, "cores": procs, "kind": "port",
-               "sample": f"every {args.ref_sample}th voxel ({s_solved} solved, {spts} points), "
-                         f"oracle store+densify+init, {wall:.1f} s wall over {procs} processes"}
+        cpu = cpu_baseline_subprocess(args)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"config4: {args.voxels}-voxel planar map per GPU ingested as "
+            "config": {"workload": f"config4: ONE {args.voxels}-voxel planar map ingested as "
                                    f"one scan ({npts} points, 0.5 m voxels, n*=81, "
                                    f"Gaussian init for all first solves)",
-                       "voxels_per_gpu": args.voxels, "points_per_gpu": npts,
-                       "solved_per_gpu": solved, "l2": "inputs 1.2 GB > 126 MB L2, no flush",
-                       "parallelism": f"hash-shard x{world}"},
+                       "voxels": args.voxels, "points": npts,
+                       "solved_per_step": float(tot_solved.item()),
+                       "l2": "inputs 1.2 GB > 126 MB L2, no flush",
+                       "parallelism": (f"hash-shard x{world}: one map, voxels owned by "
+                                       f"mix64(key) % {world}, whole scan on every rank"
+                                       if world > 1 else "single GPU")},
             "roofline": roof,
             "stage_ms": stage_ms,
             "stage_roofline": stage_roofline,
@@ -514,9 +663,19 @@ def run_gpu(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
                     "wall_ms_per_step": e2e_wall_ms / args.steps,
-                    "api": "MappingEngine.ingest_stream (pinned host frames, H2D of frame i+1 "
-                           "overlapped with frame i)"},
+                    "records_fetched_per_step": fetched["records"],
+                    "api": "MappingEngine.ingest_stream(fetch_records=True): pinned host frames "
+                           "H2D (frame i+1 overlapped with frame i), the frame's Gaussian records "
+                           "D2H into pinned host memory on a third stream (overlapped with frame "
+                           "i+1), ingest report read back" +
+                           ("; N>1: + sharded.gather_frame to rank 0 every frame" if world > 1 else "")},
+            "e2e_map_resident": {"value": float(tot_solved.item()) / (res_ms / args.steps / 1e3),
+                                 "unit": UNIT, "ms_per_step": res_ms / args.steps,
+                                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 7 * 8 * 2 + 21 * 8,
+                                 "api": "MappingEngine.ingest_stream: the round-1 e2e, outputs stay "
+                                        "in HBM (only the ingest report comes back)"},
             "gpu_launches": launches,
+            "tail": tail,
             "trajectory": traj,
             "scans": scans,
             "render": render,
@@ -538,6 +697,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--traj-scans", type=int, default=20)
     ap.add_argument("--scan-reps", type=int, default=20)
+    ap.add_argument("--tail-voxels", type=int, default=1_000_000)
+    ap.add_argument("--tail-steps", type=int, default=3)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -36,6 +36,7 @@ extern "C" {
 #define VX_E_CUDA (-3)      /* CUDA runtime failure                     */
 #define VX_E_NOMEM (-4)     /* device allocation failed                 */
 #define VX_E_RANGE (-5)     /* key outside the packed 3x21-bit lattice  */
+#define VX_E_CAPACITY (-6)  /* caller buffer too small; required size returned, state kept */
 
 /* per-problem / per-voxel status */
 #define VX_ST_OK 0
@@ -272,6 +273,15 @@ int vx_map_ingest(VxMap* map, const double* d_xyz, const double* d_rgb, int64_t 
                   const VxCamera* camera, const double* d_image, const VxSplatConfig* cfg,
                   VxGaussianOut* out, int64_t out_capacity, int64_t* out_records,
                   VxFrameInfo* frame_info, VxDensifyInfo* densify_info, void* stream);
+
+/* When vx_map_ingest returns VX_E_CAPACITY the frame HAS been stored and
+ * densified (its voxels are ACTIVE/CONVERGED) and *out_records holds the
+ * number of records its first solves need; the first-solve list is kept until
+ * the next mutating call.  Grow the buffer and call this to write them
+ * (pipeline.py:154-171: every first solve gets its Gaussians exactly once). */
+int vx_map_emit_first_gaussians(VxMap* map, const VxCamera* camera, const double* d_image,
+                                const VxSplatConfig* cfg, VxGaussianOut* out,
+                                int64_t out_capacity, int64_t* out_records, void* stream);
 
 /* `cells[key]` lookup: d_voxels[i] = voxel id of key i (-1 if absent). */
 int vx_map_lookup(VxMap* map, const int64_t* d_keys, int64_t n, int32_t* d_voxels, void* stream);

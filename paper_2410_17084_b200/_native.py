@@ -21,6 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VX_LIB_PATH") or os.path.join(_HERE, "_lib", "libvoxgpr.so")
 
 VX_OK, VX_E_INPUT, VX_E_CONTRACT, VX_E_CUDA, VX_E_NOMEM, VX_E_RANGE = 0, -1, -2, -3, -4, -5
+VX_E_CAPACITY = -6
 ST_OK, ST_DEGENERATE, ST_CHOL_FAIL = 0, 1, 2
 KERNELS = {"se": 0, "matern32": 1, "matern52": 2}
 ROT_IDENTITY, ROT_EIGEN = 0, 1
@@ -116,6 +117,8 @@ _SIGS = {
     "vx_map_ingest": ([vp, vp, vp, C.c_int64, C.POINTER(VxCamera), vp, C.POINTER(VxSplatConfig),
                        C.POINTER(VxGaussianOut), C.c_int64, c_i64p, C.POINTER(VxFrameInfo),
                        C.POINTER(VxDensifyInfo), vp], C.c_int),
+    "vx_map_emit_first_gaussians": ([vp, C.POINTER(VxCamera), vp, C.POINTER(VxSplatConfig),
+                                     C.POINTER(VxGaussianOut), C.c_int64, c_i64p, vp], C.c_int),
     "vx_map_lookup": ([vp, vp, C.c_int64, vp, vp], C.c_int),
     "vx_map_set_frame_keys": ([vp, vp, C.c_int64, vp], C.c_int),
     "vx_map_apply_prediction": ([vp, c_i64p, vp, vp, vp, C.c_int64, C.POINTER(C.c_uint8), vp],
@@ -181,6 +184,8 @@ def check(rc: int, what: str = "") -> None:
         raise errors.ContractViolationError(msg)
     if rc == VX_E_NOMEM:
         raise MemoryError(msg)
+    if rc == VX_E_CAPACITY:
+        raise BufferError(msg)
     raise RuntimeError(f"voxgpr CUDA failure: {msg}")
 
 

@@ -268,6 +268,9 @@ int map_ingest(VxMap* m, const double* xyz, const double* rgb, int64_t n, const 
                const double* image, const VxSplatConfig* scfg, VxGaussianOut* out,
                int64_t out_capacity, int64_t* out_records, VxFrameInfo* fi, VxDensifyInfo* di,
                cudaStream_t s);
+int map_emit_first_gaussians(VxMap* m, const VxCamera* cam, const double* image,
+                             const VxSplatConfig* scfg, VxGaussianOut* out, int64_t out_capacity,
+                             int64_t* out_records, cudaStream_t s);
 int map_clear(VxMap* m, cudaStream_t s);
 int map_lookup(VxMap* m, const int64_t* keys, int64_t n, int32_t* out, cudaStream_t s);
 int map_set_frame_keys(VxMap* m, const int64_t* keys, int64_t n, cudaStream_t s);
@@ -524,6 +527,17 @@ int vx_map_ingest(VxMap* map, const double* d_xyz, const double* d_rgb, int64_t 
     }
     return map_ingest(map, d_xyz, d_rgb, n, camera, d_image, cfg, out, out_capacity, out_records,
                       frame_info, densify_info, as_stream(stream));
+}
+
+int vx_map_emit_first_gaussians(VxMap* map, const VxCamera* camera, const double* d_image,
+                                const VxSplatConfig* cfg, VxGaussianOut* out,
+                                int64_t out_capacity, int64_t* out_records, void* stream) {
+    if (!map || !camera || !cfg || !out) {
+        set_error("null argument");
+        return VX_E_INPUT;
+    }
+    return map_emit_first_gaussians(map, camera, d_image, cfg, out, out_capacity, out_records,
+                                    as_stream(stream));
 }
 
 int vx_map_lookup(VxMap* map, const int64_t* d_keys, int64_t n, int32_t* d_voxels, void* stream) {

@@ -1992,9 +1992,18 @@ __device__ void team_voxel_epilogue(const VoxelSolveArgs& va, const VoxelCtx& c,
 // blockIdx.x, later ones come from an atomic counter, so CTAs that drew small
 // voxels take more of them (measured: the tile buckets 18.6 -> 18.2 ms vs the
 // static blockIdx + k * gridDim stride).  Each launch takes its own counter
-// from a ring, so launches on concurrent streams never share one.
-constexpr int TILE_CTR_RING = 1024;
+// from ONE library-wide ring (g_ctr_ring below, shared by every kernel
+// instantiation), so two launches in flight on concurrent streams get different
+// counters unless TILE_CTR_RING launches are issued while one is still running.
+constexpr int TILE_CTR_RING = 4096;
 __device__ int g_tile_ctr[TILE_CTR_RING];
+static std::atomic<unsigned> g_ctr_ring{0};
+static int next_queue_counter(int** ctr, cudaStream_t s) {
+    VX_CUDA(cudaGetSymbolAddress(reinterpret_cast<void**>(ctr), g_tile_ctr));
+    *ctr += g_ctr_ring.fetch_add(1) % TILE_CTR_RING;
+    VX_CUDA(cudaMemsetAsync(*ctr, 0, sizeof(int), s));
+    return VX_OK;
+}
 __device__ __forceinline__ int tile_next(int* s_next, int* ctr) {
     __syncthreads();
     if (threadIdx.x == 0) *s_next = int(gridDim.x) + atomicAdd(ctr, 1);
@@ -2692,11 +2701,8 @@ static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     int blocks = num_items;
     const int cap = sm_count() * per_sm;
     if (blocks > cap) blocks = cap;
-    static std::atomic<unsigned> ring{0};
     int* ctr = nullptr;
-    VX_CUDA(cudaGetSymbolAddress(reinterpret_cast<void**>(&ctr), g_tile_ctr));
-    ctr += ring.fetch_add(1) % TILE_CTR_RING;
-    VX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), s));
+    VX_TRY(next_queue_counter(&ctr, s));
     kfn<<<blocks, NW * 32, smem, s>>>(va, pa, m_max, mm, ctr);
     count_launch();
     VX_CHECK_LAUNCH();

@@ -56,6 +56,7 @@ struct VxMap {
     vx::DevBuf cflag, cscan, cand_voxel, cand_n, cand_status, cand_before, cand_after, items,
         okflag, okscan, solved_vids, cand_axis, cand_meanf;
     int64_t solve_candidates = 0, solved = 0;
+    int64_t first_count = 0;   // first solves of the last ingest, listed in `items`
     // counters (device) + pinned mirror
     vx::DevBuf counters;
     int64_t* host_counters = nullptr;
@@ -658,6 +659,7 @@ int map_densify(VxMap* m, VxDensifyInfo* info, cudaStream_t s) {
 static int map_densify_impl(VxMap* m, VxDensifyInfo* info, cudaStream_t s) {
     VxDensifyInfo di{};
     m->solve_candidates = 0;
+    m->first_count = 0;
     m->solved = 0;
     const int64_t U = m->frame_touched;
     if (U == 0) {
@@ -782,6 +784,10 @@ static int map_densify_impl(VxMap* m, VxDensifyInfo* info, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ ingest
+int map_emit_first_gaussians(VxMap* m, const VxCamera* cam, const double* image,
+                             const VxSplatConfig* scfg, VxGaussianOut* out, int64_t out_capacity,
+                             int64_t* out_records, cudaStream_t s);
+
 int map_ingest(VxMap* m, const double* xyz, const double* rgb, int64_t n, const VxCamera* cam,
                const double* image, const VxSplatConfig* scfg, VxGaussianOut* out,
                int64_t out_capacity, int64_t* out_records, VxFrameInfo* fi, VxDensifyInfo* di,
@@ -806,12 +812,27 @@ int map_ingest(VxMap* m, const double* xyz, const double* rgb, int64_t n, const 
                                       m->cand_voxel.as<int32_t>(), S, m->items.as<int32_t>());
     count_launch();
     VX_CHECK_LAUNCH();
-    const int64_t cnt = dloc.first_solves;
+    m->first_count = dloc.first_solves;
+    return map_emit_first_gaussians(m, cam, image, scfg, out, out_capacity, out_records, s);
+}
+
+// Gaussians of the last ingest's first solves (m->items, update order).  A
+// capacity shortfall is reported AFTER the frame has committed, so it must not
+// lose the records: *out_records = the required count, VX_E_CAPACITY, and the
+// list stays in m->items until the next mutating call, so the caller can grow
+// its buffer and call this again (vx_map_emit_first_gaussians).
+int map_emit_first_gaussians(VxMap* m, const VxCamera* cam, const double* image,
+                             const VxSplatConfig* scfg, VxGaussianOut* out, int64_t out_capacity,
+                             int64_t* out_records, cudaStream_t s) {
+    if (out_records) *out_records = 0;
+    const int64_t cnt = m->first_count;
+    if (cnt <= 0 || cam == nullptr || out == nullptr) return VX_OK;
     const int64_t recs = cnt * scfg->n_s * scfg->n_s;
     if (recs > out_capacity) {
+        if (out_records) *out_records = recs;
         set_error("Gaussian output capacity %lld < %lld records", (long long)out_capacity,
                   (long long)recs);
-        return VX_E_INPUT;
+        return VX_E_CAPACITY;
     }
     prof_begin(P_SPLAT, s);
     VX_TRY(launch_gaussians(m->pxyz.as<double>(), m->prgb.as<double>(), m->pvar.as<double>(),
@@ -1075,6 +1096,7 @@ int map_clear(VxMap* m, cudaStream_t s) {
     m->num_slots = 0;
     m->frame_touched = 0;
     m->solve_candidates = 0;
+    m->first_count = 0;
     m->solved = 0;
     m->frame_index = -1;
     if (m->tcap > 0) {

@@ -48,7 +48,7 @@ class IngestReport:
 class MappingEngine:
     def __init__(self, config: PipelineConfig, *, shard_rank: int = 0, shard_world: int = 1,
                  voxel_capacity: int = 0, point_capacity: int = 0, gaussian_capacity: int = 0,
-                 record_log: bool = False):
+                 record_log: bool = False, track_order: bool = False):
         self.config = config
         self.vmap = VoxelMap.from_config(config, shard_rank=shard_rank, shard_world=shard_world,
                                          voxel_capacity=voxel_capacity,
@@ -59,6 +59,13 @@ class MappingEngine:
         self.pending = []        # device int32 tensors of first-solved voxel ids
         self._pending_n = 0
         self._pinned = {}
+        # track_order: a global order key per record, (frame << 32) | index of the
+        # voxel's first point in the frame that first-solved it, taken when the
+        # voxel is solved (not when its records are emitted), so sharded outputs
+        # can be merged back into the single-GPU order (sharding.py)
+        self.track_order = bool(track_order)
+        self._orders = []        # device int64 tensors, one per record batch
+        self._pending_keys = []  # order keys of the pending voxels (threshold > 1)
 
     # -- buffers ------------------------------------------------------------
     def _ensure_records(self, need: int):
@@ -72,7 +79,8 @@ class MappingEngine:
             for k in ("position", "scale", "rotation", "opacity", "color", "source_key"):
                 getattr(new, k)[:n].copy_(getattr(self.records, k)[:n])
         self.records = new
-        torch.cuda.current_stream().synchronize()
+        # device-wide: the old buffer may still be read by a D2H on another stream
+        torch.cuda.synchronize()
 
     def _stage(self, name, arr):
         """Copy a host array into a reusable pinned buffer, then H2D (async)."""
@@ -86,6 +94,65 @@ class MappingEngine:
         host.numpy()[:] = a.reshape(-1)
         return host.view(*a.shape).to(N.device(), non_blocking=True)
 
+    def _first_solves(self, frame_index: int):
+        """(voxel ids, order keys) of the last densify's first solves, update order."""
+        v = self.vmap.device_view()
+        S = int(v.solve_candidates)
+        st = N.view_tensor(v.solve_status, (S,), np.uint8)
+        bf = N.view_tensor(v.solve_state_before, (S,), np.uint8)
+        vids = N.view_tensor(v.solve_voxels, (S,), np.int32)
+        first = vids[(st == N.ST_OK) & (bf == 1)].clone()
+        keys = None
+        if self.track_order:
+            lf = N.view_tensor(v.last_first, (int(v.num_voxels),), np.int32)
+            keys = (int(frame_index) << 32) | lf.index_select(0, first.long()).long()
+        return first, keys
+
+    def _append_orders(self, keys):
+        import torch
+        if keys is not None and keys.numel():
+            self._orders.append(torch.repeat_interleave(keys, self.config.n_s * self.config.n_s))
+
+    def record_order(self):
+        """Order keys of the records `gaussians_device()` returns (track_order)."""
+        import torch
+        if not self.track_order:
+            raise RuntimeError("MappingEngine(track_order=True) is required")
+        if not self._orders:
+            return torch.empty(0, dtype=torch.int64, device=N.device())
+        if len(self._orders) > 1:
+            self._orders = [torch.cat(self._orders)]
+        return self._orders[0]
+
+    def frame_predictions(self) -> dict:
+        """The last densify's predictions as device tensors, in update order.
+
+        `densify_frame`'s `list[VoxelPrediction]` (gpr.py:269-311) without the
+        host objects: keys (S,3) int64, order (S,) int64 ((frame << 32) | first
+        point index, the global merge key of sharded outputs), positions (S,M,3),
+        colors (S,M,3), variances (S,M) of the S voxels solved in the frame.
+        """
+        import torch
+        v = self.vmap.device_view()
+        S, M = int(v.solved), int(v.pred_points)
+        V = int(v.num_voxels)
+        dev = N.device()
+        if S == 0:
+            return {"keys": torch.empty((0, 3), dtype=torch.int64, device=dev),
+                    "order": torch.empty(0, dtype=torch.int64, device=dev),
+                    "positions": torch.empty((0, M, 3), dtype=torch.float64, device=dev),
+                    "colors": torch.empty((0, M, 3), dtype=torch.float64, device=dev),
+                    "variances": torch.empty((0, M), dtype=torch.float64, device=dev)}
+        vids = N.view_tensor(v.solved_voxels, (S,), np.int32).long()
+        slot = N.view_tensor(v.pred_slot, (V,), np.int32).index_select(0, vids).long()
+        nslot = int(slot.max().item()) + 1
+        lf = N.view_tensor(v.last_first, (V,), np.int32).index_select(0, vids).long()
+        return {"keys": N.view_tensor(v.keys, (V, 3), np.int64).index_select(0, vids),
+                "order": (int(v.frame_index) << 32) | lf,
+                "positions": N.view_tensor(v.pred_xyz, (nslot, M, 3), np.float64).index_select(0, slot),
+                "colors": N.view_tensor(v.pred_rgb, (nslot, M, 3), np.float64).index_select(0, slot),
+                "variances": N.view_tensor(v.pred_var, (nslot, M), np.float64).index_select(0, slot)}
+
     # -- ingest -------------------------------------------------------------
     def ingest(self, positions, colors, camera=None, image=None) -> IngestReport:
         """Host-array ingest: H2D of the scan (and image), then `ingest_device`."""
@@ -97,7 +164,8 @@ class MappingEngine:
         rep.duration_s = time.perf_counter() - t0
         return rep
 
-    def ingest_stream(self, frames, reset_each: bool = False) -> list:
+    def ingest_stream(self, frames, reset_each: bool = False, on_frame=None,
+                      fetch_records: bool = False, on_records=None) -> list:
         """Ingest a sequence of host frames with H2D double-buffering.
 
         `frames` yields (positions, colors, camera, image) with positions /
@@ -105,17 +173,30 @@ class MappingEngine:
         image an (H, W, 3) float64 host tensor or None.  The copy of frame k+1
         runs on a side stream while frame k is processed, so a steady stream
         costs max(H2D, device work) per frame instead of their sum.
+
+        `on_frame(report)` runs after each frame's ingest (e.g. the sharded
+        gather).  `fetch_records`: the Gaussian records each frame adds (the
+        GaussianMap the reference's ingest_frame produces on the host,
+        pipeline.py:161-171) are copied D2H into pinned host memory on a third
+        stream, overlapped with the next frame's device work;
+        `on_records(report, host_fields)` receives them once they have landed
+        (the dict's tensors are reused two frames later: copy what you keep).
         """
         import torch
         dev = N.device()
         compute = torch.cuda.current_stream()
         if getattr(self, "_copier", None) is None:
-            # persistent side stream + double buffers (allocated once, reused)
+            # persistent side streams + double buffers (allocated once, reused)
             self._copier = torch.cuda.Stream(device=dev)
+            self._d2h = torch.cuda.Stream(device=dev)
             self._bufs = [dict(), dict()]
             self._free = [None, None]
+            self._hrec = [dict(), dict()]
+            self._drec = [None, None]
+            self._drec_free = [None, None]
         copier, bufs, free = self._copier, self._bufs, self._free
         reports = []
+        waiting = []            # (report, d2h-done event, host fields)
         it = iter(frames)
 
         def issue(frame, slot):
@@ -139,6 +220,35 @@ class MappingEngine:
                 ready.record(copier)
             return (b["xyz"], b["rgb"], int(pos.shape[0]), cam, b["img"], ready)
 
+        def fetch(rep, first, slot):
+            n = self.num_gaussians - first
+            done = torch.cuda.Event()
+            host = self._hrec[slot]
+            src = {k: v[first:first + n] for k, v in self.gaussians_device().items()} if n else {}
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            with torch.cuda.stream(self._d2h):
+                self._d2h.wait_event(ev)
+                out = {}
+                for k, t in src.items():
+                    h = host.get(k)
+                    if h is None or h.shape[0] < n:
+                        h = torch.empty((max(n, 1024),) + tuple(t.shape[1:]), dtype=t.dtype).pin_memory()
+                        host[k] = h
+                    out[k] = h[:n]
+                    out[k].copy_(t, non_blocking=True)
+                done.record(self._d2h)
+            if reset_each:
+                self._drec_free[slot] = done   # the device records may be rewritten after this
+            waiting.append((rep, done, out))
+
+        def drain(keep: int):
+            while len(waiting) > keep:
+                rep, done, out = waiting.pop(0)
+                done.synchronize()
+                if on_records is not None:
+                    on_records(rep, out)
+
         nxt = next(it, None)
         pending = issue(nxt, 0) if nxt is not None else None
         k = 0
@@ -149,11 +259,27 @@ class MappingEngine:
             compute.wait_event(ready)
             if reset_each:
                 self.reset()
-            reports.append(self.ingest_device(dx, dc, n, cam, di))
+                if fetch_records:
+                    # double-buffered device records: frame k writes one buffer while
+                    # the D2H of frame k-1 reads the other
+                    self.records = self._drec[k & 1]
+                    if self._drec_free[k & 1] is not None:
+                        compute.wait_event(self._drec_free[k & 1])
+            first = self.num_gaussians
+            rep = self.ingest_device(dx, dc, n, cam, di)
+            if reset_each and fetch_records:
+                self._drec[k & 1] = self.records
+            reports.append(rep)
+            if on_frame is not None:
+                on_frame(rep)
+            if fetch_records:
+                fetch(rep, first, k & 1)
+                drain(1)
             done = torch.cuda.Event()
             done.record(compute)
             free[k & 1] = done
             k += 1
+        drain(0)
         return reports
 
     def ingest_device(self, d_xyz, d_rgb, n: int, camera=None, d_image=None) -> IngestReport:
@@ -167,8 +293,13 @@ class MappingEngine:
         fi, di = N.VxFrameInfo(), N.VxDensifyInfo()
         added = 0
         if cfg.expansion_threshold <= 1 and camera is not None:
-            worst = nsub * (n // max(cfg.tau, 1) + 1)
-            self._ensure_records(self.num_gaussians + worst)
+            # first guess for the record buffer: every touched voxel of this frame
+            # can be a first solve (voxels left at tau-1 points by earlier
+            # frames, or READY after a failed solve, need one new point each), so
+            # the guess is only a guess; a shortfall is reported after the frame
+            # has committed and the records are emitted into a grown buffer below
+            guess = nsub * (n // max(cfg.tau, 1) + 1)
+            self._ensure_records(self.num_gaussians + guess)
             out = self.records.out_struct(self.num_gaussians)
             cam, sc = N.camera_struct(camera), N.splat_struct(
                 cfg.n_s, cfg.n_r, cfg.weight_floor, cfg.scale_floor, cfg.initial_opacity,
@@ -180,9 +311,19 @@ class MappingEngine:
                                    C.byref(fi), C.byref(di), N.stream_ptr())
             vm._mutated()
             vm._frame_serial += 1
+            if rc == N.VX_E_CAPACITY:
+                # the frame is stored and densified; its first-solve list is kept
+                # by the library until the next mutating call
+                self._ensure_records(self.num_gaussians + int(written.value))
+                out = self.records.out_struct(self.num_gaussians)
+                rc = lib.vx_map_emit_first_gaussians(
+                    vm._h(), C.byref(cam), N.ptr(d_image), C.byref(sc), C.byref(out),
+                    self.records.count - self.num_gaussians, C.byref(written), N.stream_ptr())
             N.check(rc)
             added = int(written.value)
             self.num_gaussians += added
+            if self.track_order and added:
+                self._append_orders(self._first_solves(fi.frame_index)[1])
         else:
             rc = lib.vx_map_store_frame(vm._h(), N.ptr(d_xyz), N.ptr(d_rgb), int(n), C.byref(fi),
                                         N.stream_ptr())
@@ -193,27 +334,31 @@ class MappingEngine:
             vm._mutated()
             N.check(rc)
             if di.first_solves:
-                v = vm.device_view()
-                S = int(v.solve_candidates)
-                st = N.view_tensor(v.solve_status, (S,), np.uint8)
-                bf = N.view_tensor(v.solve_state_before, (S,), np.uint8)
-                vids = N.view_tensor(v.solve_voxels, (S,), np.int32)
-                first = vids[(st == N.ST_OK) & (bf == 1)].clone()
+                first, keys = self._first_solves(fi.frame_index)
                 self.pending.append(first)
+                if keys is not None:
+                    self._pending_keys.append(keys)
                 self._pending_n += len(first)
-            if camera is not None and self._pending_n and \
-                    self._pending_n >= cfg.expansion_threshold:
+            if camera is not None and self._expand_now(self._pending_n):
                 added = self._expand(camera, d_image)
         return IngestReport(frame_index=int(fi.frame_index), points_stored=int(n),
                             voxels_touched=int(fi.touched), voxels_solved=int(di.solved),
                             newly_active=int(di.first_solves), newly_converged=int(di.converged),
                             primitives_added=added, duration_s=time.perf_counter() - t0)
 
+    def _expand_now(self, pending: int) -> bool:
+        """pipeline.py:158-159: expand once `expansion_threshold` voxels are pending
+        (ShardedEngine replaces this with the count over all shards)."""
+        return pending > 0 and pending >= self.config.expansion_threshold
+
     def _expand(self, camera, d_image) -> int:
+        if not self._pending_n:
+            return 0
         import torch
         cfg = self.config
         vids = torch.cat(self.pending).contiguous()
-        self.pending, self._pending_n = [], 0
+        keys = torch.cat(self._pending_keys) if self._pending_keys else None
+        self.pending, self._pending_n, self._pending_keys = [], 0, []
         recs = len(vids) * cfg.n_s * cfg.n_s
         self._ensure_records(self.num_gaussians + recs)
         out = self.records.out_struct(self.num_gaussians)
@@ -223,6 +368,7 @@ class MappingEngine:
                                                      C.byref(cam), N.ptr(d_image), C.byref(sc),
                                                      C.byref(out), N.stream_ptr()))
         self.num_gaussians += recs
+        self._append_orders(keys)
         return recs
 
     # -- outputs ------------------------------------------------------------
@@ -242,4 +388,5 @@ class MappingEngine:
     def reset(self):
         self.vmap.clear()
         self.num_gaussians = 0
-        self.pending, self._pending_n = [], 0
+        self.pending, self._pending_n, self._pending_keys = [], 0, []
+        self._orders = []

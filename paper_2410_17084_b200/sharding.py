@@ -8,14 +8,19 @@ rank receives the whole scan by H2D from pinned host memory, keeps only its
 keys in its own device map and never exchanges data on the hot path (no
 data-path collective; weak scaling).
 
-The only collective is the optional hand-off of the Gaussian records to a
-consumer rank (`gather_records`): an all-gather of per-rank counts, a padded
-gather of the SoA fields over NCCL (gloo on CPU for the tests), and a stable
-sort by the record order key (frame << 32 | first point index of the voxel in
-that frame).  Because single-GPU records are emitted in first-solve update
-order — i.e. ascending first-touch point index within a frame
-(voxel_map.py:324-326, pipeline.py:154-171) — the gathered map is identical,
-record for record, to the single-GPU map.
+The only collective is the hand-off of the outputs to a consumer rank
+(SURVEY §8(e)): the frame's predictions (81 points x (xyz, rgb, variance) per
+solved voxel) and its Gaussian records.  `gather_v` is a gather-v: an
+all-gather of the per-rank counts, then ONE grouped batch of point-to-point
+transfers (`dist.batch_isend_irecv` = ncclGroupStart / ncclSend x fields /
+ncclRecv x (ranks x fields) / ncclGroupEnd over NVLink) straight into the
+consumer's output slices — no padding, no intermediate copies.  The consumer
+then restores the single-GPU order with one stable sort by the order key
+((frame << 32) | index of the voxel's first point in the frame, taken when the
+voxel is solved).  Single-GPU outputs are in update order = ascending first
+point index within a frame (voxel_map.py:324-326, gpr.py:281-310,
+pipeline.py:154-171), so the gathered predictions and records are identical,
+bit for bit and in order, to an unsharded run.
 """
 
 from __future__ import annotations
@@ -59,80 +64,151 @@ def owner_of(keys, world: int) -> np.ndarray:
     return (h % np.uint64(world)).astype(np.int64)
 
 
-def gather_records(rec: dict, order, dst: int = 0, group=None):
-    """Gather per-rank Gaussian record SoA tensors to `dst`, in global order.
+def _staged(t, backend: str):
+    """gloo moves host tensors only: stage device tensors through the host."""
+    return t.cpu() if backend == "gloo" and t.is_cuda else t
 
-    `rec` maps field name -> tensor with the record count as leading dim;
-    `order` is an int64 tensor of record order keys.  Returns the merged dict
-    on `dst` (None elsewhere).  Works with NCCL (device tensors) and gloo
-    (host tensors).
+
+def gather_v(fields: dict, order, dst: int = 0, group=None):
+    """Gather per-rank row sets to `dst` and merge them into global order.
+
+    `fields` maps name -> tensor whose leading dimension is this rank's row
+    count; `order` (int64, same rows) is the merge key.  Returns the merged
+    dict (rows sorted stably by `order`; the key itself under "order") on
+    `dst`, None elsewhere.  NCCL moves device tensors rank to rank over NVLink;
+    under gloo (CPU tests) the same calls move host tensors.
     """
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    backend = dist.get_backend(group)
     dev = order.device
-    n = torch.tensor([order.numel()], dtype=torch.int64, device=dev)
+    cdev = torch.device("cpu") if backend == "gloo" else dev
+    n = torch.tensor([order.numel()], dtype=torch.int64, device=cdev)
     counts = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(counts, n, group=group)
     counts = [int(c.item()) for c in counts]
-    cap = max(counts) if counts else 0
-    out = {}
-    for name in sorted(rec) + ["__order__"]:
-        t = order if name == "__order__" else rec[name]
-        pad = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-        pad[: t.shape[0]] = t
-        bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
-        dist.gather(pad, bufs, dst=dst, group=group)
-        if rank == dst:
-            out[name] = torch.cat([b[:c] for b, c in zip(bufs, counts)])
+    names = sorted(fields) + ["order"]
+    src = dict(fields, order=order)
+    ops = []
+    out = None
+    if rank == dst:
+        total = sum(counts)
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        out = {}
+        for nm in names:
+            t = src[nm]
+            out[nm] = torch.empty((total,) + tuple(t.shape[1:]), dtype=t.dtype, device=cdev)
+            out[nm][offs[rank]:offs[rank + 1]] = _staged(t, backend)
+        for r in range(world):
+            if r == rank or counts[r] == 0:
+                continue
+            for nm in names:
+                ops.append(dist.P2POp(dist.irecv, out[nm][offs[r]:offs[r + 1]],
+                                      dist.get_global_rank(group, r) if group else r, group))
+    elif counts[rank]:
+        keep = []
+        for nm in names:
+            t = _staged(src[nm].contiguous(), backend)
+            keep.append(t)
+            ops.append(dist.P2POp(dist.isend, t,
+                                  dist.get_global_rank(group, dst) if group else dst, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
     if rank != dst:
         return None
-    perm = torch.sort(out.pop("__order__"), stable=True).indices
-    return {k: v.index_select(0, perm) for k, v in out.items()}
+    key = out.pop("order")
+    perm = torch.sort(key, stable=True).indices
+    res = {k: v.index_select(0, perm) for k, v in out.items()}
+    res["order"] = key.index_select(0, perm)
+    if backend == "gloo" and dev.type == "cuda":
+        res = {k: v.to(dev) for k, v in res.items()}
+    return res
+
+
+def gather_records(rec: dict, order, dst: int = 0, group=None):
+    """Gaussian record SoA fields of every rank -> `dst`, in global order."""
+    out = gather_v(rec, order, dst=dst, group=group)
+    if out is not None:
+        out.pop("order")
+    return out
 
 
 class ShardedEngine:
-    """MappingEngine on rank `rank` of `world`: owns mix64(key) % world == rank."""
+    """MappingEngine on rank `rank` of `world`: owns mix64(key) % world == rank.
 
-    def __init__(self, config, rank: int, world: int, **kw):
+    Every rank ingests the whole scan (its hashing kernel keeps only owned
+    keys); `gather_frame` hands the frame's predictions and new Gaussian
+    records to the consumer rank, `gather` the whole Gaussian map.
+    """
+
+    def __init__(self, config, rank: int, world: int, group=None, **kw):
         self.rank, self.world = rank, world
-        self.engine = MappingEngine(config, shard_rank=rank, shard_world=world, **kw)
-        self.orders = []
+        self.engine = MappingEngine(config, shard_rank=rank, shard_world=world,
+                                    track_order=True, **kw)
+        self._frame_first_record = 0
+        self.group = group
+        if world > 1:
+            # expansion_threshold counts pending voxels over the WHOLE map
+            # (pipeline.py:157-159): every shard expands when the global count
+            # reaches it, so the records match an unsharded run
+            self.engine._expand_now = self._expand_now
+
+    def _expand_now(self, pending: int) -> bool:
+        import torch
+        import torch.distributed as dist
+        from . import _native as N
+        dev = torch.device("cpu") if dist.get_backend(self.group) == "gloo" else N.device()
+        t = torch.tensor([pending], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, group=self.group)
+        total = int(t.item())
+        return total > 0 and total >= self.engine.config.expansion_threshold
 
     def ingest(self, positions, colors, camera=None, image=None):
-        before = self.engine.num_gaussians
-        rep = self.engine.ingest(positions, colors, camera, image)
-        self._record_order(before, rep)
-        return rep
+        self._frame_first_record = self.engine.num_gaussians
+        return self.engine.ingest(positions, colors, camera, image)
 
-    def _record_order(self, before: int, rep):
+    def ingest_device(self, d_xyz, d_rgb, n, camera=None, d_image=None):
+        self._frame_first_record = self.engine.num_gaussians
+        return self.engine.ingest_device(d_xyz, d_rgb, n, camera, d_image)
+
+    def reset(self):
+        self.engine.reset()
+        self._frame_first_record = 0
+
+    def _records(self, lo: int = 0):
         import torch
         from . import _native as N
-        added = self.engine.num_gaussians - before
-        if added == 0:
-            return
-        v = self.engine.vmap.device_view()
-        S = int(v.solve_candidates)
-        st = N.view_tensor(v.solve_status, (S,), np.uint8)
-        bf = N.view_tensor(v.solve_state_before, (S,), np.uint8)
-        vids = N.view_tensor(v.solve_voxels, (S,), np.int32)
-        first = vids[(st == N.ST_OK) & (bf == 1)].long()
-        lf = N.view_tensor(v.last_first, (int(v.num_voxels),), np.int32)
-        key = (int(rep.frame_index) << 32) | lf.index_select(0, first).long()
-        nsub = self.engine.config.n_s ** 2
-        self.orders.append(torch.repeat_interleave(key, nsub))
-
-    def gather(self, dst: int = 0, group=None):
-        import torch
-        dev = self.engine.records.position.device if self.engine.records is not None else None
         recs = self.engine.gaussians_device()
-        order = torch.cat(self.orders) if self.orders else torch.empty(0, dtype=torch.int64,
-                                                                        device=dev)
+        dev = N.device()
         if not recs:
             recs = {k: torch.empty((0,) + s, dtype=dt, device=dev) for k, s, dt in (
                 ("position", (3,), torch.float64), ("scale", (3,), torch.float64),
                 ("rotation", (4,), torch.float64), ("opacity", (), torch.float64),
                 ("color", (3,), torch.float64), ("source_key", (3,), torch.int64))}
+        order = self.engine.record_order()
+        return {k: v[lo:] for k, v in recs.items()}, order[lo:]
+
+    def gather_frame(self, dst: int = 0, group=None) -> dict | None:
+        """The last frame's outputs on `dst`, identical to an unsharded run.
+
+        {"predictions": {keys, order, positions, colors, variances} of every
+        voxel solved in the frame (update order), "gaussians": the records the
+        frame added (position, scale, rotation, opacity, color, source_key)}.
+        """
+        pred = self.engine.frame_predictions()
+        order = pred.pop("order")
+        p = gather_v(pred, order, dst=dst, group=group)
+        recs, rorder = self._records(self._frame_first_record)
+        g = gather_records(recs, rorder, dst=dst, group=group)
+        if p is None:
+            return None
+        return {"predictions": p, "gaussians": g}
+
+    def gather(self, dst: int = 0, group=None):
+        """Every Gaussian record of the sharded map on `dst`, in global order."""
+        recs, order = self._records(0)
         return gather_records(recs, order, dst=dst, group=group)

@@ -643,7 +643,14 @@ class VoxelMap:
         rows = torch.repeat_interleave(off, count) + (
             torch.arange(int(count.sum().item()), device=keys.device)
             - torch.repeat_interleave(torch.cumsum(count, 0) - count, count))
-        pk = torch.floor(xyz[rows] / self.voxel_size).long()
+        # keys of the stored points by the hashing kernel's own arithmetic (IEEE
+        # division + floor, vx_voxel_keys); torch's `xyz / scalar` on CUDA is a
+        # multiply by the reciprocal and can misplace points on a lattice face
+        pts = xyz[rows].contiguous()
+        pk = torch.empty((len(pts), 3), dtype=torch.int64, device=keys.device)
+        if len(pts):
+            N.check(self._lib.vx_voxel_keys(N.ptr(pts), len(pts), float(self.voxel_size),
+                                            N.ptr(pk), N.stream_ptr()))
         bad = (pk != keys[owner]).any(dim=1)
         per = torch.zeros(V, dtype=torch.int64, device=keys.device).index_add_(0, owner, bad.long())
         idx = torch.nonzero(per).flatten().cpu().numpy()

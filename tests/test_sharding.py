@@ -80,3 +80,55 @@ def test_ordered_gather_world2_gloo():
     n = 301
     np.testing.assert_array_equal(pos, np.arange(n * 3, dtype=np.float64).reshape(n, 3))
     np.testing.assert_array_equal(keys, np.arange(n * 3, dtype=np.int64).reshape(n, 3))
+
+
+def _worker_v(rank, world, port, q, empty_rank):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # a frame's predictions split by owner (81-point blocks per voxel), one
+        # rank owning nothing: gather-v of unequal, possibly empty row sets
+        rng = np.random.default_rng(11)
+        n, m = 157, 81
+        order = np.sort(rng.choice(1 << 40, n, replace=False)).astype(np.int64)
+        owner = rng.integers(0, world, n)
+        owner[owner == empty_rank] = (empty_rank + 1) % world
+        mine = owner == rank
+        pos = np.arange(n * m * 3, dtype=np.float64).reshape(n, m, 3)
+        var = np.arange(n * m, dtype=np.float64).reshape(n, m) * 0.5
+        keys = np.arange(n * 3, dtype=np.int64).reshape(n, 3) - 7
+        out = sharding.gather_v({"positions": torch.from_numpy(pos[mine]),
+                                 "variances": torch.from_numpy(var[mine]),
+                                 "keys": torch.from_numpy(keys[mine])},
+                                torch.from_numpy(order[mine]), dst=world - 1)
+        if rank == world - 1:
+            q.put({k: v.numpy() for k, v in out.items()})
+        else:
+            assert out is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,empty_rank", [(2, 0), (3, 1)])
+def test_gather_v_unequal_counts_and_empty_rank(world, empty_rank):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_v, args=(r, world, port, q, empty_rank))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, m = 157, 81
+    rng = np.random.default_rng(11)
+    order = np.sort(rng.choice(1 << 40, n, replace=False)).astype(np.int64)
+    np.testing.assert_array_equal(out["order"], order)
+    np.testing.assert_array_equal(out["positions"],
+                                  np.arange(n * m * 3, dtype=np.float64).reshape(n, m, 3))
+    np.testing.assert_array_equal(out["variances"],
+                                  np.arange(n * m, dtype=np.float64).reshape(n, m) * 0.5)
+    np.testing.assert_array_equal(out["keys"], np.arange(n * 3, dtype=np.int64).reshape(n, 3) - 7)

@@ -238,6 +238,11 @@ def render_image(scene: OutdoorScene, cam: Pinhole):
 # points-per-voxel histogram of the config-1 scan at 0.5 m
 N_BINS = ((10, 16), (16, 32), (32, 64), (64, 128), (128, 160))
 N_PROBS = (0.56, 0.29, 0.06, 0.085, 0.005)
+# ... and of the Livox-style rosette scan (config 3, the tail variant of config
+# 4): [10,16,32,64,128,256,512,743) = [144,170,85,39,26,10,12] of 486 solvable
+# voxels, max n 742
+TAIL_BINS = ((10, 16), (16, 32), (32, 64), (64, 128), (128, 256), (256, 512), (512, 743))
+TAIL_PROBS = (144, 170, 85, 39, 26, 10, 12)
 
 
 def planar_map(n_voxels=1_000_000, voxel_size=0.5, seed=0, shuffle=True,
