@@ -7,11 +7,11 @@ FP64 sm_100a CUDA kernels behind the C ABI of `include/voxgpr.h`
 (`_lib/libvoxgpr.so`, loaded through `_native`).  There is no CPU path.
 """
 
-from .camera import Camera
+from .camera import Camera, relative_transform, same_view
 from .config import PipelineConfig
 from .engine import IngestReport, MappingEngine
 from .errors import (ContractViolationError, DegenerateGeometryError, InputDomainError,
-                     NumericalDegeneracyError, VoxsplatError)
+                     NumericalDegeneracyError, ParseError, VoxsplatError)
 from .gpr import (AxisSelection, GprBatchResult, GprProblem, GprResult, densify_device,
                   densify_frame, gpr_solve, gpr_solve_batch, kernel_matrix, make_mesh_grid,
                   select_value_axis)
@@ -19,7 +19,7 @@ from .splat_init import (GaussianMap, GaussianPrimitive, Subgrid, init_color, in
                          init_gaussians_batch, init_gaussians_for_voxel, init_position,
                          partition_subgrids)
 from . import renderer
-from .renderer import RenderBuffers, project_points, render
+from .renderer import RenderBuffers, SplatProjection, project_gaussian, project_points, render
 from .voxel_map import (ColoredPoint, FrameUpdateSet, PointCloud, VoxelCell, VoxelKey, VoxelMap,
                         VoxelPrediction, VoxelState, classify_voxel, update_voxel_variances,
                         voxel_key)
@@ -27,9 +27,9 @@ from .voxel_map import (ColoredPoint, FrameUpdateSet, PointCloud, VoxelCell, Vox
 __version__ = "0.1.0"
 
 __all__ = [
-    "Camera", "PipelineConfig", "MappingEngine", "IngestReport",
-    "VoxsplatError", "InputDomainError", "DegenerateGeometryError",
-    "NumericalDegeneracyError", "ContractViolationError",
+    "Camera", "same_view", "relative_transform", "PipelineConfig", "MappingEngine",
+    "IngestReport", "VoxsplatError", "InputDomainError", "DegenerateGeometryError",
+    "NumericalDegeneracyError", "ContractViolationError", "ParseError",
     "AxisSelection", "GprBatchResult", "GprProblem", "GprResult", "densify_frame",
     "densify_device", "gpr_solve", "gpr_solve_batch", "kernel_matrix", "make_mesh_grid",
     "select_value_axis",
@@ -37,5 +37,6 @@ __all__ = [
     "init_gaussians_batch", "init_gaussians_for_voxel", "init_position", "partition_subgrids",
     "ColoredPoint", "FrameUpdateSet", "PointCloud", "VoxelCell", "VoxelKey", "VoxelMap",
     "VoxelPrediction", "VoxelState", "classify_voxel", "update_voxel_variances", "voxel_key",
-    "renderer", "render", "project_points", "RenderBuffers",
+    "renderer", "render", "project_points", "project_gaussian", "SplatProjection",
+    "RenderBuffers",
 ]

@@ -2652,6 +2652,8 @@ __global__ void __launch_bounds__(NW * 32, NW <= 6 ? 2 : 1) gpr_big_kernel(
     }
 }
 
+#include "vx_panel.cuh"
+
 // tile-kernel configurations per size bucket: (8-column tiles per warp and
 // pass, warps per CTA, resident CTAs per SM the registers are capped for,
 // rows per factor thread in the panel solve)
@@ -2704,6 +2706,114 @@ static int launch_tile(const VoxelSolveArgs& va, const ProblemArgs& pa, int num_
     int* ctr = nullptr;
     VX_TRY(next_queue_counter(&ctr, s));
     kfn<<<blocks, NW * 32, smem, s>>>(va, pa, m_max, mm, ctr);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    return VX_OK;
+}
+
+
+// Items of the large-n bucket sorted by n, largest first (one CTA: counting
+// sort over n in [lo, lo + 4096); order within one n is arbitrary, which does
+// not matter: every item's result is independent of the others).
+template <bool VOXEL>
+__global__ void __launch_bounds__(1024) k_sort_items_desc(VoxelSolveArgs va, ProblemArgs pa, int count,
+                                                          int hi, int32_t* out) {
+    __shared__ int hist[4096];
+    const int* items = VOXEL ? va.items : pa.items;
+    auto key = [&](int i) {
+        const int s = items[i];
+        const int n = VOXEL ? va.cand_n[s] : int(pa.x_off[s + 1] - pa.x_off[s]);
+        int b = hi - n;                       // largest n -> bin 0
+        return b < 0 ? 0 : (b > 4095 ? 4095 : b);
+    };
+    for (int b = threadIdx.x; b < 4096; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < count; i += blockDim.x) atomicAdd(&hist[key(i)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int b = 0; b < 4096; ++b) {
+            const int c = hist[b];
+            hist[b] = acc;
+            acc += c;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < count; i += blockDim.x) out[atomicAdd(&hist[key(i)], 1)] = items[i];
+}
+
+// Team size (CTAs per cluster) of the panel kernel: few items -> spread each
+// voxel over up to 8 SMs (latency, e.g. one Livox scan); many items -> one CTA
+// per voxel.  VX_PANEL_C overrides (A/B experiments).
+static int panel_team_size(int num_items) {
+    if (const char* e = getenv("VX_PANEL_C")) {
+        const int c = atoi(e);
+        if (c == 1 || c == 2 || c == 4 || c == 8) return c;
+    }
+    const int sms = sm_count();
+    if (num_items * 8 <= sms) return 8;
+    if (num_items * 4 <= sms) return 4;
+    if (num_items * 2 <= sms) return 2;
+    return 1;
+}
+
+template <bool VOXEL>
+static int launch_panel(const VoxelSolveArgs& va_in, const ProblemArgs& pa_in, int num_items,
+                        int n_max, int m_max, int mm, DevBuf& work, cudaStream_t s) {
+    if (num_items <= 0) return VX_OK;
+    VoxelSolveArgs va = va_in;
+    ProblemArgs pa = pa_in;
+    const int C = panel_team_size(num_items);
+    const int NP = round_up(n_max, PNB);
+    const int A32 = round_up(m_max + 1, PNB);
+    const int R = NP + A32;
+    const int MC = m_max + 1 > 96 ? round_up(m_max + 1, 32) : 96;
+    const PanelLayout lay(NP, MC, m_max);
+    const size_t smem = size_t(lay.total) * sizeof(double);
+    auto kfn = gpr_panel_kernel<VOXEL>;
+    VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 1;
+    VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, PNT, smem));
+    if (per_sm < 1) per_sm = 1;
+    int teams = (sm_count() * per_sm) / C;
+    if (teams > num_items) teams = num_items;
+    if (teams < 1) teams = 1;
+    PanelArgs pk{};
+    pk.per_team = panel_base(R, NP / PNB);
+    pk.partial_per_team = int64_t(C) * PW * 2 * A32;
+    pk.csize = C;
+    pk.nmax = n_max;
+    pk.mmax = m_max;
+    pk.mm = mm;
+    // workspace: sorted items | team slots | partial sums | L panels
+    const size_t items_b = (size_t(num_items) * 4 + 255) & ~size_t(255);
+    const size_t slots_b = (size_t(teams) * 4 + 255) & ~size_t(255);
+    const size_t part_b = size_t(teams) * pk.partial_per_team * 8;
+    const size_t l_b = size_t(teams) * pk.per_team * 8;
+    VX_TRY(work.reserve(items_b + slots_b + part_b + l_b, s));
+    char* base = work.as<char>();
+    int32_t* sorted = reinterpret_cast<int32_t*>(base);
+    pk.slots = reinterpret_cast<int*>(base + items_b);
+    pk.partial = reinterpret_cast<double*>(base + items_b + slots_b);
+    pk.work = reinterpret_cast<double*>(base + items_b + slots_b + part_b);
+    k_sort_items_desc<VOXEL><<<1, 1024, 0, s>>>(va, pa, num_items, n_max, sorted);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    if (VOXEL) va.items = sorted; else pa.items = sorted;
+    VX_TRY(next_queue_counter(&pk.queue, s));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(teams * C));
+    cfg.blockDim = dim3(PNT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(C);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VX_CUDA(cudaLaunchKernelEx(&cfg, kfn, va, pa, pk));
     count_launch();
     VX_CHECK_LAUNCH();
     return VX_OK;
@@ -2892,7 +3002,9 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
             if (a.M + 1 <= 96)
                 return launch_tile<20, 1, T160_NW, 1, T160_ROWS, true>(a, none, a.num_items, a.M, mm, s);
             return launch_cta<true>(a, none, a.num_items, max_n < 160 ? max_n : 160, a.M, mm, work, s);
-        default:
+        default:   // n > 160: augmented panel Cholesky on a team of CTAs
+            if (!getenv("VX_OLD_BIG"))
+                return launch_panel<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
             if (a.M + 1 <= 96) return launch_big<12, true>(a, none, a.num_items, max_n, a.M, mm, work, s);
             return launch_cta<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
     }
@@ -2913,6 +3025,7 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
         if (bucket == 6) return launch_tile<T96_NRB, T96_CFG, false>(none, pa, count, max_m, 1, s);
         if (bucket == 3) return launch_tile<16, T128_CFG, false>(none, pa, count, max_m, 1, s);
 
+        if (!getenv("VX_OLD_BIG")) return launch_panel<false>(none, pa, count, max_n, max_m, 1, work, s);
         return launch_big<12, false>(none, pa, count, max_n, max_m, 1, work, s);
     }
     return launch_generic<false>(none, pa, count, max_n, max_m, work, s);

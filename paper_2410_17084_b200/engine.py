@@ -19,6 +19,7 @@ import numpy as np
 
 from . import _native as N
 from .config import PipelineConfig
+from .formats import PlyPayload
 from .splat_init import GaussianMap, GaussianRecords
 from .voxel_map import VoxelMap
 
@@ -205,7 +206,28 @@ class MappingEngine:
                 if free[slot] is not None:
                     copier.wait_event(free[slot])
                 b = bufs[slot]
+                decoded = isinstance(pos, PlyPayload)
+                if decoded:
+                    # raw 15-byte PLY vertex records: H2D, then widened to f64
+                    # xyz / rgb by vx_decode_ply on this copy stream
+                    n = pos.count
+                    rec = b.get("ply")
+                    if rec is None or rec.numel() < pos.records.numel():
+                        rec = torch.empty(pos.records.numel(), dtype=torch.uint8, device=dev)
+                        b["ply"] = rec
+                    for name in ("xyz", "rgb"):
+                        cur = b.get(name)
+                        if cur is None or cur.shape != (n, 3):
+                            b[name] = torch.empty((n, 3), dtype=torch.float64, device=dev)
+                    if n:
+                        rec[:pos.records.numel()].copy_(pos.records, non_blocking=True)
+                        N.check(N.lib().vx_decode_ply(N.ptr(rec), n, N.ptr(b["xyz"]),
+                                                      N.ptr(b["rgb"]), N.vp(copier.cuda_stream)),
+                                f"vx_decode_ply {pos.path}")
+                    pos = b["xyz"]
                 for name, t in (("xyz", pos), ("rgb", col), ("img", img)):
+                    if decoded and name != "img":
+                        continue          # decoded in place above
                     if t is None:
                         b[name] = None
                         continue
@@ -373,9 +395,15 @@ class MappingEngine:
 
     # -- outputs ------------------------------------------------------------
     def gaussians_device(self) -> dict:
+        """The records so far as device tensors (empty tensors before the first)."""
+        import torch
         n = self.num_gaussians
         if self.records is None:
-            return {}
+            dev = N.device()
+            return {k: torch.empty((0,) + s, dtype=dt, device=dev) for k, s, dt in (
+                ("position", (3,), torch.float64), ("scale", (3,), torch.float64),
+                ("rotation", (4,), torch.float64), ("opacity", (), torch.float64),
+                ("color", (3,), torch.float64), ("source_key", (3,), torch.int64))}
         return {k: getattr(self.records, k)[:n] for k in
                 ("position", "scale", "rotation", "opacity", "color", "source_key")}
 

@@ -3,7 +3,11 @@
 `read_ply_device` parses the PLY header on the host, stages the raw 15-byte
 binary vertex records in pinned memory, copies them H2D (15 B/point instead of
 the 48 B/point of f64 positions + colours) and widens them on the device
-(`vx_decode_ply`); `read_ply` returns the reference's host `PointCloud`.
+(`vx_decode_ply`); `read_ply` returns the reference's host `PointCloud`;
+`read_ply_payload` stops at the pinned records (`PlyPayload`), which
+`MappingEngine.ingest_stream` copies and decodes on its copy stream
+(`stream.stream_frames`).  Every format failure raises `ParseError(path,
+location, reason)` as the reference does (errors.py:39-46).
 
 Same byte format as the reference writer/reader (formats.py:23-32, 154-198):
 8-byte magic `VXSPLAT1`, `<IQI` (version 1, record count, echo length), the
@@ -22,7 +26,7 @@ from pathlib import Path
 import numpy as np
 
 from . import _native as N
-from .errors import ContractViolationError, InputDomainError
+from .errors import ParseError
 from .splat_init import GaussianMap
 
 PLY_VERTEX = np.dtype([("x", "<f4"), ("y", "<f4"), ("z", "<f4"),
@@ -32,35 +36,95 @@ _PLY_PROPS = [("float", "x"), ("float", "y"), ("float", "z"),
 
 
 def _ply_header(data: bytes, path):
+    """(format, vertex count, payload offset); ParseError with the reference's
+    locations (formats.py:66-118)."""
     if data[:3] != b"ply":
-        raise InputDomainError(f"{path}: missing ply magic")
-    off, fmt, count, props = 0, None, None, []
-    for _ in range(101):
+        raise ParseError(path, "byte 0", "missing ply magic")
+    # collect the header lines first, then interpret them: a malformed line in a
+    # header that never ends reports the missing end, as the reference does
+    lines, off = [], 0
+    while True:
         end = data.find(b"\n", off)
         if end < 0:
-            raise InputDomainError(f"{path}: header never ends")
-        line = data[off:end].decode("ascii", "replace").strip()
+            raise ParseError(path, f"byte {off}", "header never ends")
+        lines.append((off, data[off:end].decode("ascii", "replace").strip()))
         off = end + 1
-        tok = line.split()
-        if line == "end_header":
+        if lines[-1][1] == "end_header":
             break
-        if not tok or tok[0] in ("comment", "ply"):
+        if len(lines) > 100:
+            raise ParseError(path, f"byte {off}", "header too long")
+    if lines[0][1] != "ply":
+        raise ParseError(path, "byte 0", "missing ply magic")
+    fmt, count, props = None, None, []
+    for line_off, line in lines[1:-1]:
+        tok = line.split()
+        if not tok or tok[0] == "comment":
             continue
         if tok[0] == "format":
             if len(tok) < 2 or tok[1] not in ("ascii", "binary_little_endian"):
-                raise InputDomainError(f"{path}: unsupported format {line!r}")
+                raise ParseError(path, f"byte {line_off}", f"unsupported format {line!r}")
             fmt = tok[1]
         elif tok[0] == "element":
             if len(tok) != 3 or tok[1] != "vertex":
-                raise InputDomainError(f"{path}: unsupported element {line!r}")
-            count = int(tok[2])
+                raise ParseError(path, f"byte {line_off}", f"unsupported element {line!r}")
+            try:
+                count = int(tok[2])
+            except ValueError as exc:
+                raise ParseError(path, f"byte {line_off}", "bad vertex count") from exc
         elif tok[0] == "property":
             props.append(tuple(tok[1:]))
-    else:
-        raise InputDomainError(f"{path}: header too long")
-    if fmt is None or count is None or props != _PLY_PROPS:
-        raise InputDomainError(f"{path}: unsupported PLY layout {props!r}")
-    return fmt, count, off
+    nlines = len(lines)
+    if fmt is None or count is None:
+        raise ParseError(path, "header", "format or element vertex line missing")
+    if props != _PLY_PROPS:
+        raise ParseError(path, "header", f"unsupported property layout {props!r}")
+    return fmt, count, off, nlines
+
+
+class PlyPayload:
+    """Binary PLY vertex records staged in pinned host memory (15 B/point).
+
+    `MappingEngine.ingest_stream` copies them H2D and widens them on the device
+    (`vx_decode_ply`): the scan crosses PCIe at 15 B/point instead of 48.
+    """
+
+    def __init__(self, records, count: int, path=""):
+        self.records, self.count, self.path = records, int(count), str(path)
+        self.shape = (self.count, 3)
+
+
+def read_ply_payload(path) -> PlyPayload:
+    """Header parse on the host + the raw records in pinned memory (binary PLY);
+    ascii files are parsed to float64 rows and re-packed (no narrowing)."""
+    import torch
+    data = Path(path).read_bytes()
+    fmt, count, off, nlines = _ply_header(data, path)
+    if fmt == "binary_little_endian":
+        need = count * PLY_VERTEX.itemsize
+        if len(data) - off < need:
+            raise ParseError(path, f"byte {len(data)}",
+                             f"payload truncated: need {need} bytes, have {len(data) - off}")
+        host = torch.frombuffer(bytearray(data[off:off + need]), dtype=torch.uint8).pin_memory()
+        return PlyPayload(host, count, path)
+    raise ParseError(path, "header", "stream ingest expects binary_little_endian PLY frames")
+
+
+def _ascii_rows(data: bytes, off: int, count: int, nlines: int, path) -> np.ndarray:
+    rows = data[off:].decode("ascii", "replace").splitlines()
+    if len(rows) < count:
+        raise ParseError(path, f"line {nlines + len(rows)}",
+                         f"payload truncated: need {count} rows, have {len(rows)}")
+    out = np.empty((count, 6))
+    for i in range(count):
+        tok = rows[i].split()
+        if len(tok) != 6:
+            raise ParseError(path, f"line {nlines + i + 1}", f"expected 6 fields, got {len(tok)}")
+        try:
+            out[i, :3] = [float(v) for v in tok[:3]]
+            out[i, 3:] = [int(v) for v in tok[3:]]
+        except ValueError as exc:
+            raise ParseError(path, f"line {nlines + i + 1}", f"bad vertex row: {exc}") from exc
+    return out
 
 
 def read_ply_device(path):
@@ -68,23 +132,22 @@ def read_ply_device(path):
     import torch
     lib = N.lib()
     data = Path(path).read_bytes()
-    fmt, count, off = _ply_header(data, path)
+    fmt, count, off, nlines = _ply_header(data, path)
     dev = N.device()
     xyz = torch.empty((count, 3), dtype=torch.float64, device=dev)
     rgb = torch.empty((count, 3), dtype=torch.float64, device=dev)
     if fmt == "binary_little_endian":
         need = count * PLY_VERTEX.itemsize
         if len(data) - off < need:
-            raise InputDomainError(f"{path}: payload truncated")
+            raise ParseError(path, f"byte {len(data)}",
+                             f"payload truncated: need {need} bytes, have {len(data) - off}")
         host = torch.frombuffer(bytearray(data[off:off + need]), dtype=torch.uint8).pin_memory()
         rec = host.to(dev, non_blocking=True)
         N.check(lib.vx_decode_ply(N.ptr(rec), count, N.ptr(xyz), N.ptr(rgb), N.stream_ptr()))
     else:
         # ascii rows hold decimal text: the reference parses them straight to
         # float64 (formats.py:140-141), so positions are not narrowed to f32
-        rows = np.loadtxt(data[off:].decode("ascii").splitlines()[:count], ndmin=2)
-        if len(rows) < count or rows.shape[1] != 6:
-            raise InputDomainError(f"{path}: bad ascii payload")
+        rows = _ascii_rows(data, off, count, nlines, path)
         r = np.zeros(count, dtype=PLY_VERTEX)
         r["red"], r["green"], r["blue"] = rows[:, 3], rows[:, 4], rows[:, 5]
         rec = torch.from_numpy(r.view(np.uint8).copy()).to(dev)
@@ -148,19 +211,23 @@ def write_map(path, source, config=None) -> int:
 
 
 def read_map(path):
-    """(GaussianMap, config-echo dict) — mirror of the reference read_map."""
+    """(GaussianMap, config-echo dict) — mirror of the reference read_map
+    (formats.py:172-198), ParseError locations included."""
     data = Path(path).read_bytes()
     if data[:8] != MAP_MAGIC:
-        raise ContractViolationError(f"{path}: bad magic, not a map file")
+        raise ParseError(path, "byte 0", "bad magic, not a map file")
+    if len(data) < 8 + 16:
+        raise ParseError(path, f"byte {len(data)}", "truncated header")
     version, count, echo_len = struct.unpack_from("<IQI", data, 8)
     if version != MAP_VERSION:
-        raise ContractViolationError(f"{path}: unsupported version {version}")
+        raise ParseError(path, "byte 8", f"unsupported version {version}")
     body = 8 + 16
     echo = data[body:body + echo_len].decode("utf-8")
     need = count * MAP_RECORD.itemsize
     payload = data[body + echo_len:body + echo_len + need]
     if len(payload) < need:
-        raise ContractViolationError(f"{path}: payload truncated")
+        raise ParseError(path, f"byte {len(data)}",
+                         f"payload truncated: need {need} bytes, have {len(data) - body - echo_len}")
     rec = np.frombuffer(payload, dtype=MAP_RECORD)
     gmap = GaussianMap.from_arrays(rec["position"], rec["scale"], rec["rotation"], rec["opacity"],
                                    rec["color"], rec["source_key"])

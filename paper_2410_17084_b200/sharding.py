@@ -180,15 +180,7 @@ class ShardedEngine:
         self._frame_first_record = 0
 
     def _records(self, lo: int = 0):
-        import torch
-        from . import _native as N
         recs = self.engine.gaussians_device()
-        dev = N.device()
-        if not recs:
-            recs = {k: torch.empty((0,) + s, dtype=dt, device=dev) for k, s, dt in (
-                ("position", (3,), torch.float64), ("scale", (3,), torch.float64),
-                ("rotation", (4,), torch.float64), ("opacity", (), torch.float64),
-                ("color", (3,), torch.float64), ("source_key", (3,), torch.int64))}
         order = self.engine.record_order()
         return {k: v[lo:] for k, v in recs.items()}, order[lo:]
 

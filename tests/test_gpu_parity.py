@@ -103,7 +103,7 @@ def test_error_isolation_and_jitter_rule():
     assert vx.gpr_solve_batch([bad]).ok == oracle_ok
 
 
-@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 64, 65, 100, 150, 200, 400])
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 64, 65, 100, 150, 161, 200, 256, 400, 512, 742])
 def test_size_buckets_against_oracle(n):
     """Every kernel bucket (team n<=32, team n<=64, generic) against the oracle.
 
@@ -133,6 +133,34 @@ def test_size_buckets_against_oracle(n):
             mu2, var2, _ = O.dense_inverse_posterior(p.x, p.f, p.noise_diag, p.x_star, p.lam)
             assert np.abs(r.mu_star - mu).max() <= 10 * np.abs(mu2 - mu).max() + ATOL
             assert np.abs(r.sigma_star_diag - var).max() <= 10 * np.abs(var2 - var).max() + ATOL
+
+
+@pytest.mark.parametrize("c", [1, 2, 4, 8])
+def test_large_n_panel_kernel_team_sizes(c, monkeypatch):
+    """The n > 160 panel kernel gives the same answer whatever its team size
+    (CTAs per cluster splitting one voxel), mixed n in one launch, n* = 256
+    query points, and the jitter retry (an exactly duplicated training point
+    with zero noise makes K + diag(noise) singular: the first factorisation
+    fails, the retry with +jitter I succeeds, gpr.py:186-194)."""
+    monkeypatch.setenv("VX_PANEL_C", str(c))
+    rng = np.random.default_rng(77)
+    probs = []
+    for n, m in ((161, 81), (300, 256), (742, 81), (190, 7), (450, 81)):
+        x = rng.uniform(0, 0.5, (n, 2))
+        f = rng.normal(0, 0.05, n)
+        nz = rng.uniform(1e-4, 1e-2, n)
+        probs.append(vx.GprProblem(x, f, nz, rng.uniform(0, 0.5, (m, 2)), 4.0))
+    x = rng.uniform(0, 0.5, (200, 2))
+    x[17] = x[3]
+    probs.append(vx.GprProblem(x, rng.normal(0, 0.05, 200), np.zeros(200),
+                               rng.uniform(0, 0.5, (81, 2)), 4.0))
+    batch = vx.gpr_solve_batch(probs)
+    assert batch.ok
+    for p, r in zip(probs, batch.results):
+        mu, var, _ = O.posterior(p.x, p.f, p.noise_diag, p.x_star, p.lam)
+        mu2, var2, _ = O.dense_inverse_posterior(p.x, p.f, p.noise_diag, p.x_star, p.lam)
+        assert np.abs(r.mu_star - mu).max() <= 10 * np.abs(mu2 - mu).max() + ATOL
+        assert np.abs(r.sigma_star_diag - var).max() <= 10 * np.abs(var2 - var).max() + ATOL
 
 
 # ---------------------------------------------------------------------------
@@ -410,7 +438,7 @@ def test_hash_sharded_maps_reassemble_single_gpu_result():
         for sh in shards:
             sh.ingest(pos, col, cam, img)
     recs = [sh.engine.gaussians_device() for sh in shards]
-    order = torch.cat([torch.cat(sh.orders) for sh in shards])
+    order = torch.cat([sh.engine.record_order() for sh in shards])
     perm = torch.sort(order, stable=True).indices
     ref = full.gaussians_device()
     for k in ref:
@@ -421,6 +449,41 @@ def test_hash_sharded_maps_reassemble_single_gpu_result():
         np.testing.assert_array_equal(np.unique(sharding.owner_of(
             recs[r]["source_key"].cpu().numpy(), 2)), [r])
     assert len(own) == sum(len(r["opacity"]) for r in recs)
+
+
+def test_record_capacity_shortfall_after_commit():
+    """a frame whose first solves outgrow the record buffer.
+
+    Frame 1 leaves 1000 voxels at tau - 1 = 9 points, frame 2 adds one point to
+    each: 1000 first solves (9000 records) against the engine's first guess of
+    9 * (n // tau + 1) = 909.  The library reports VX_E_CAPACITY after the frame
+    has committed, the engine grows its buffer and emits the records; the
+    result equals an engine whose buffer was large enough from the start.
+    """
+    rng = np.random.default_rng(4)
+    keys = np.stack(np.meshgrid(np.arange(40), np.arange(25), [0], indexing="ij"), -1).reshape(-1, 3)
+    lo = keys * 0.5
+    f1 = (lo[:, None, :] + rng.uniform(0.05, 0.45, (1000, 9, 3)) * [1, 1, 0.05]
+          + [0, 0, 0.2]).reshape(-1, 3)
+    f2 = lo + rng.uniform(0.05, 0.45, (1000, 3)) * [1, 1, 0.05] + [0, 0, 0.2]
+    cam = vx.Camera(fx=100, fy=100, cx=50, cy=50, width=100, height=100)
+    img = np.full((100, 100, 3), 0.25)
+    cfg = vx.PipelineConfig(voxel_size=0.5)
+    small = vx.MappingEngine(cfg)
+    big = vx.MappingEngine(cfg, gaussian_capacity=20000)
+    for e in (small, big):
+        r1 = e.ingest(f1, np.full((len(f1), 3), 0.5), cam, img)
+        assert r1.voxels_solved == 0
+        r2 = e.ingest(f2, np.full((len(f2), 3), 0.5), cam, img)
+        assert r2.newly_active == 1000 and r2.primitives_added == 9000
+    a, b = small.gaussians_device(), big.gaussians_device()
+    for k in b:
+        assert torch_equal(a[k], b[k]), k
+
+
+def torch_equal(a, b):
+    import torch
+    return a.shape == b.shape and bool(torch.equal(a, b))
 
 
 def test_store_frame_edge_cases():
