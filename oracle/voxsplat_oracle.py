@@ -440,6 +440,33 @@ def ingest(omap: OracleMap, positions, colors, cfg: DensifyConfig,
             "gaussians": gauss}
 
 
+class OraclePipeline:
+    """pipeline.py:139-171 with the expansion threshold: first solves queue in
+    `pending` (update order, pipeline.py:154-156) and are expanded — from their
+    CURRENT prediction (`cell.last_prediction`, a re-fit may have replaced the
+    first one) with the expanding frame's camera and image — once at least
+    `threshold` voxels are pending (pipeline.py:157-171)."""
+
+    def __init__(self, omap: OracleMap, cfg: DensifyConfig, threshold: int = 1):
+        self.omap, self.cfg, self.threshold = omap, cfg, int(threshold)
+        self.pending = []
+
+    def ingest(self, positions, colors, camera, image):
+        omap = self.omap
+        update = omap.store_frame(positions, colors)
+        first = {k for k in update if omap.cells[k].state == READY}
+        preds, skipped = densify(update, omap, self.cfg)
+        self.pending.extend(p["key"] for p in preds if p["key"] in first)
+        gauss = []
+        if self.pending and len(self.pending) >= self.threshold:
+            for key in self.pending:
+                gauss.append(gaussians_for_prediction(omap.cells[key].pred, camera, image,
+                                                      self.cfg.n_s, self.cfg.n_r))
+            self.pending = []
+        return {"update": update, "predictions": preds, "skipped": skipped, "gaussians": gauss,
+                "first": first}
+
+
 # ---------------------------------------------------------------------------
 # Forward splat renderer (renderer.py:90-207) — restated per primitive in a
 # plain loop over pixels of its bbox rows (no patch broadcasting), checked

@@ -18,7 +18,7 @@ from .gpr import (AxisSelection, GprBatchResult, GprProblem, GprResult, densify_
 from .splat_init import (GaussianMap, GaussianPrimitive, Subgrid, init_color, init_covariance,
                          init_gaussians_batch, init_gaussians_for_voxel, init_position,
                          partition_subgrids)
-from . import renderer
+from . import formats, renderer, stream
 from .renderer import RenderBuffers, SplatProjection, project_gaussian, project_points, render
 from .voxel_map import (ColoredPoint, FrameUpdateSet, PointCloud, VoxelCell, VoxelKey, VoxelMap,
                         VoxelPrediction, VoxelState, classify_voxel, update_voxel_variances,
@@ -37,6 +37,6 @@ __all__ = [
     "init_gaussians_batch", "init_gaussians_for_voxel", "init_position", "partition_subgrids",
     "ColoredPoint", "FrameUpdateSet", "PointCloud", "VoxelCell", "VoxelKey", "VoxelMap",
     "VoxelPrediction", "VoxelState", "classify_voxel", "update_voxel_variances", "voxel_key",
-    "renderer", "render", "project_points", "project_gaussian", "SplatProjection",
+    "formats", "stream", "renderer", "render", "project_points", "project_gaussian", "SplatProjection",
     "RenderBuffers",
 ]

@@ -97,58 +97,14 @@ __global__ void k_mesh_grid(const double* ext, int64_t P, int n_s, int n_r, doub
     out[e * 2 + 1] = xadd(lo1, xdiv(xmul(double(sc * n_r + fc) + 0.5, xsub(hi1, lo1)), double(mm)));
 }
 
-// select_value_axis (gpr.py:57-78), one warp per point set
+// select_value_axis (gpr.py:57-78), one thread per point set (pca_value_axis)
 __global__ void k_select_axis(const double* pts, const int64_t* off, int64_t P, int8_t* axis_out) {
-    const int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p >= P) return;
     const int64_t b = off[p];
-    const int n = int(off[p + 1] - b);
     const double* P3 = pts + b * 3;
-    if (n < 3) {
-        if (lane == 0) axis_out[p] = -1;
-        return;
-    }
-    double mx = 0, my = 0, mz = 0;
-    if (lane == 0) {
-        for (int r = 0; r < n; ++r) {
-            mx = xadd(mx, P3[r * 3]);
-            my = xadd(my, P3[r * 3 + 1]);
-            mz = xadd(mz, P3[r * 3 + 2]);
-        }
-        mx = xdiv(mx, double(n));
-        my = xdiv(my, double(n));
-        mz = xdiv(mz, double(n));
-    }
-    mx = __shfl_sync(FULL, mx, 0);
-    my = __shfl_sync(FULL, my, 0);
-    mz = __shfl_sync(FULL, mz, 0);
-    double c[6] = {0, 0, 0, 0, 0, 0};
-    for (int r = lane; r < n; r += 32) {
-        double dx = xsub(P3[r * 3], mx), dy = xsub(P3[r * 3 + 1], my), dz = xsub(P3[r * 3 + 2], mz);
-        c[0] = fma(dx, dx, c[0]);
-        c[1] = fma(dx, dy, c[1]);
-        c[2] = fma(dx, dz, c[2]);
-        c[3] = fma(dy, dy, c[3]);
-        c[4] = fma(dy, dz, c[4]);
-        c[5] = fma(dz, dz, c[5]);
-    }
-    for (int k = 0; k < 6; ++k)
-        for (int o = 16; o > 0; o >>= 1) c[k] += __shfl_xor_sync(FULL, c[k], o);
-    if (lane == 0) {
-        for (int k = 0; k < 6; ++k) c[k] /= double(n);
-        double ev[3], v0[3];
-        eig3_sym(c, ev, v0, nullptr);
-        int ax = -1;
-        if (!(ev[2] <= 1e-18 || ev[1] <= 1e-9 * ev[2])) {
-            double w0 = fabs(v0[0]), w1 = fabs(v0[1]), w2 = fabs(v0[2]);
-            ax = 2;
-            double best = w2;
-            if (w1 > best) { ax = 1; best = w1; }
-            if (w0 > best) { ax = 0; }
-        }
-        axis_out[p] = int8_t(ax);
-    }
+    axis_out[p] = int8_t(pca_value_axis([&](int r) { return P3 + int64_t(r) * 3; },
+                                        int(off[p + 1] - b)));
 }
 
 // problem-mode bucketing for gpr_solve_batch
@@ -356,7 +312,7 @@ int vx_select_axis_batch(const double* d_points, const int64_t* d_offsets, int64
                          void* stream) {
     if (num <= 0) return VX_OK;
     cudaStream_t s = as_stream(stream);
-    k_select_axis<<<unsigned((num * 32 + 255) / 256), 256, 0, s>>>(d_points, d_offsets, num, d_axis);
+    k_select_axis<<<unsigned((num + 127) / 128), 128, 0, s>>>(d_points, d_offsets, num, d_axis);
     count_launch();
     VX_CHECK_LAUNCH();
     return VX_OK;

@@ -233,6 +233,49 @@ __device__ inline void eig3_sym(const double c[6],  // xx, xy, xz, yy, yz, zz
     }
 }
 
+// select_value_axis (gpr.py:57-78) of n points given by `pt(r)` (a pointer to
+// xyz): centred covariance / n, smallest eigenvector, the degeneracy test of
+// gpr.py:73-74 and the argmax with ties preferring z, then y (gpr.py:75-77).
+// Returns -1 for a degenerate set.  THE one routine both device routes use
+// (vx_select_axis_batch and the densify PCA prepass), so they cannot
+// disagree: means by sequential accumulation (NumPy reduces axis 0 row by
+// row), covariance entries by sequential FMA accumulation.
+template <typename PointFn>
+__device__ __forceinline__ int pca_value_axis(PointFn pt, int n) {
+    if (n < 3) return -1;
+    double mx = 0.0, my = 0.0, mz = 0.0;
+    for (int r = 0; r < n; ++r) {
+        const double* p = pt(r);
+        mx = xadd(mx, p[0]);
+        my = xadd(my, p[1]);
+        mz = xadd(mz, p[2]);
+    }
+    mx = xdiv(mx, double(n));
+    my = xdiv(my, double(n));
+    mz = xdiv(mz, double(n));
+    double c[6] = {0, 0, 0, 0, 0, 0};
+    for (int r = 0; r < n; ++r) {
+        const double* p = pt(r);
+        const double dx = xsub(p[0], mx), dy = xsub(p[1], my), dz = xsub(p[2], mz);
+        c[0] = fma(dx, dx, c[0]);
+        c[1] = fma(dx, dy, c[1]);
+        c[2] = fma(dx, dz, c[2]);
+        c[3] = fma(dy, dy, c[3]);
+        c[4] = fma(dy, dz, c[4]);
+        c[5] = fma(dz, dz, c[5]);
+    }
+    for (int k = 0; k < 6; ++k) c[k] = xdiv(c[k], double(n));
+    double ev[3], v0[3];
+    eig3_sym(c, ev, v0, nullptr);
+    if (ev[2] <= 1e-18 || ev[1] <= 1e-9 * ev[2]) return -1;
+    const double w0 = fabs(v0[0]), w1 = fabs(v0[1]), w2 = fabs(v0[2]);
+    int ax = 2;
+    double best = w2;
+    if (w1 > best) { ax = 1; best = w1; }
+    if (w0 > best) ax = 0;
+    return ax;
+}
+
 // value axis -> ordered pair of parameter axes (gpr.py:36)
 __host__ __device__ __forceinline__ int param_axis_a(int ax) { return ax == 0 ? 1 : (ax == 1 ? 2 : 0); }
 __host__ __device__ __forceinline__ int param_axis_b(int ax) { return ax == 0 ? 2 : (ax == 1 ? 0 : 1); }

@@ -98,41 +98,7 @@ __global__ void __launch_bounds__(128) k_pca_prepass(VoxelSolveArgs a, int S, lo
     const int cnt = a.raw_count[vid];
     const int64_t off = a.raw_offset[vid];
     const int slot = a.pred_slot[vid];
-    int ax = -1;
-    if (n >= 3) {
-        // pts.mean(axis=0): sequential accumulation (NumPy reduces axis 0 row by row)
-        double mx = 0.0, my = 0.0, mz = 0.0;
-        for (int r = 0; r < n; ++r) {
-            const double* p = train_point(a, r, cnt, off, slot);
-            mx = xadd(mx, p[0]);
-            my = xadd(my, p[1]);
-            mz = xadd(mz, p[2]);
-        }
-        mx = xdiv(mx, double(n));
-        my = xdiv(my, double(n));
-        mz = xdiv(mz, double(n));
-        double c[6] = {0, 0, 0, 0, 0, 0};
-        for (int r = 0; r < n; ++r) {
-            const double* p = train_point(a, r, cnt, off, slot);
-            const double dx = xsub(p[0], mx), dy = xsub(p[1], my), dz = xsub(p[2], mz);
-            c[0] = fma(dx, dx, c[0]);
-            c[1] = fma(dx, dy, c[1]);
-            c[2] = fma(dx, dz, c[2]);
-            c[3] = fma(dy, dy, c[3]);
-            c[4] = fma(dy, dz, c[4]);
-            c[5] = fma(dz, dz, c[5]);
-        }
-        for (int k = 0; k < 6; ++k) c[k] /= double(n);
-        double ev[3], v0[3];
-        eig3_sym(c, ev, v0, nullptr);
-        if (!(ev[2] <= 1e-18 || ev[1] <= 1e-9 * ev[2])) {     // gpr.py:73-74
-            const double w0 = fabs(v0[0]), w1 = fabs(v0[1]), w2 = fabs(v0[2]);
-            ax = 2;                                              // ties prefer z, then y
-            double best = w2;
-            if (w1 > best) { ax = 1; best = w1; }
-            if (w0 > best) ax = 0;
-        }
-    }
+    const int ax = pca_value_axis([&](int r) { return train_point(a, r, cnt, off, slot); }, n);
     a.cand_axis[s] = int8_t(ax);
     if (ax < 0) {
         a.cand_status[s] = VX_ST_DEGENERATE;

@@ -25,10 +25,10 @@
 // L lives in a per-team global workspace, panel by panel (panel p holds rows
 // [32p, R) of its 32 columns, column-major, ld = R - 32p): 2.7 MB at n = 742,
 // L2-resident for the teams in flight.  The GEMM of phase A and the
-// triangular update of phase B are split over all warps of the team in 32x32
-// row tiles; the 32x32 diagonal block is factored redundantly by one warp of
-// every CTA (row per lane, left-looking, failure rule of dpotrf: a pivot that
-// is not > 0 fails), so the only cross-CTA synchronisation is two cluster
+// triangular update of phase B are split over all warps of the team in 16x32
+// row tiles (two CTAs per SM); the 32x32 diagonal block is factored redundantly by one warp of
+// every CTA (row per lane in shared memory, left-looking, failure rule of
+// dpotrf: a pivot that is not > 0 fails), so the only cross-CTA synchronisation is two cluster
 // barriers per panel.  A team takes voxels from the launch's atomic queue
 // (largest first, the items are sorted by n before the launch).
 
@@ -37,7 +37,9 @@
 constexpr int PNB = 32;          // panel width
 constexpr int PW = 8;            // warps per CTA
 constexpr int PNT = PW * 32;
-constexpr int PLD = 36;          // leading dimension of the 32x32 blocks in shared memory
+constexpr int PLD = 36;          // row stride of L_dd^-1 in shared memory (B fragments: 4 mod 16)
+constexpr int PLDL = 33;         // row stride of L_dd (row-per-lane reads: odd)
+constexpr int PRT = 16;          // rows per warp tile
 
 struct PanelArgs {
     double* work;                // per-team workspaces
@@ -91,7 +93,7 @@ __device__ __forceinline__ unsigned cluster_rank() {
 }
 
 template <bool VOXEL>
-__global__ void __launch_bounds__(PNT, 1) gpr_panel_kernel(VoxelSolveArgs va, ProblemArgs pa,
+__global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, ProblemArgs pa,
                                                            PanelArgs pk) {
     extern __shared__ __align__(16) double smem[];
     const int C = pk.csize;
@@ -206,41 +208,61 @@ __global__ void __launch_bounds__(PNT, 1) gpr_panel_kernel(VoxelSolveArgs va, Pr
                 const int j = p * PNB;
                 double* Pp = Lw + panel_base(R, p);
                 const int ldp = R - j;
-                // ---- phase A: P = M[j:, j:j+32] - L[j:, :j] L[j:j+32, :j]^T, 32x32 tiles
-                const int T = (R - j) / PNB;
+                // ---- phase A: P = M[j:, j:j+32] - L[j:, :j] L[j:j+32, :j]^T in 16x32
+                // row tiles (two 8-row DMMA tiles x four 8-column tiles per warp)
+                const int T = (R - j) / PRT;
                 const int nw = C * PW;
                 const int gw = (crank * PW + warp + p) % nw;
                 for (int t = gw; t < T; t += nw) {
-                    const int r0 = j + t * PNB;
-                    double acc[4][4][2];
+                    const int r0 = j + t * PRT;
+                    double acc[2][4][2];
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < 2; ++a)
 #pragma unroll
                         for (int b = 0; b < 4; ++b)
 #pragma unroll
                             for (int e = 0; e < 2; ++e)
                                 acc[a][b][e] = mval(r0 + 8 * a + g, j + 8 * b + 2 * tig + e, jit);
-                    for (int q = 0; q < p; ++q) {
+                    // k runs over the finished panels q < p (columns 32q .. 32q+31);
+                    // software-pipelined: the fragments of step s+1 load while the
+                    // DMMAs of step s issue
+                    const int steps = p * (PNB / 4);
+                    auto frag_ptr = [&](int st, int row0) {
+                        const int q = st >> 3, kk = (st & 7) * 4;
                         const int ldq = R - q * PNB;
-                        const double* Pq = Lw + panel_base(R, q) + int64_t(tig) * ldq;
-                        const double* pa_ = Pq + (r0 - q * PNB) + g;
-                        const double* pb_ = Pq + (j - q * PNB) + g;
-#pragma unroll 2
-                        for (int kk = 0; kk < PNB; kk += 4) {
-                            double fa[4], fb[4];
+                        return Lw + panel_base(R, q) + int64_t(kk + tig) * ldq + (row0 - q * PNB) + g;
+                    };
+                    double fa[2], fb[4];
+                    if (steps > 0) {
+                        const double* pa_ = frag_ptr(0, r0);
+                        const double* pb_ = frag_ptr(0, j);
+                        fa[0] = __ldcg(pa_);
+                        fa[1] = __ldcg(pa_ + 8);
 #pragma unroll
-                            for (int a = 0; a < 4; ++a) fa[a] = -__ldcg(pa_ + int64_t(kk) * ldq + 8 * a);
+                        for (int b = 0; b < 4; ++b) fb[b] = __ldcg(pb_ + 8 * b);
+                    }
+                    for (int st = 0; st < steps; ++st) {
+                        double na[2] = {0.0, 0.0}, nb[4] = {0.0, 0.0, 0.0, 0.0};
+                        if (st + 1 < steps) {
+                            const double* pa_ = frag_ptr(st + 1, r0);
+                            const double* pb_ = frag_ptr(st + 1, j);
+                            na[0] = __ldcg(pa_);
+                            na[1] = __ldcg(pa_ + 8);
 #pragma unroll
-                            for (int b = 0; b < 4; ++b) fb[b] = __ldcg(pb_ + int64_t(kk) * ldq + 8 * b);
-#pragma unroll
-                            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                                for (int b = 0; b < 4; ++b) dmma_acc(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+                            for (int b = 0; b < 4; ++b) nb[b] = __ldcg(pb_ + 8 * b);
                         }
+#pragma unroll
+                        for (int a = 0; a < 2; ++a)
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) dmma_acc(acc[a][b][0], acc[a][b][1], -fa[a], fb[b]);
+                        fa[0] = na[0];
+                        fa[1] = na[1];
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) fb[b] = nb[b];
                     }
                     double* dst = Pp + (r0 - j) + g;
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < 2; ++a)
 #pragma unroll
                         for (int b = 0; b < 4; ++b)
 #pragma unroll
@@ -248,51 +270,45 @@ __global__ void __launch_bounds__(PNT, 1) gpr_panel_kernel(VoxelSolveArgs va, Pr
                                 __stcg(dst + int64_t(8 * b + 2 * tig + e) * ldp + 8 * a, acc[a][b][e]);
                 }
                 team_sync(C);
-                // ---- phase B (1): every CTA factors the diagonal block (warp 0, row per lane)
+                // ---- phase B (1): every CTA factors the diagonal block (warp 0).
+                // Left-looking, row r by lane r, rows in shared memory (LD, stride
+                // PLDL: conflict-free row reads); then column c of L_dd^-1 by lane c
+                // into LI (row-major).  A pivot that is not > 0 fails (dpotrf).
                 if (warp == 0) {
-                    double l[PNB];
-#pragma unroll
-                    for (int c = 0; c < PNB; ++c) l[c] = __ldcg(Pp + int64_t(c) * ldp + lane);
+                    double* myrow = LD + lane * PLDL;
+#pragma unroll 4
+                    for (int c = 0; c < PNB; ++c) myrow[c] = __ldcg(Pp + int64_t(c) * ldp + lane);
+                    __syncwarp();
                     bool good = true;
-#pragma unroll
                     for (int c = 0; c < PNB; ++c) {
-                        // s = P(lane, c) - sum_{k < c} L(lane, k) L(c, k), L(c, k) from LD (row c)
-                        double s0 = l[c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-                        const double* rowc = LD + c * PLD;
-#pragma unroll
-                        for (int k = 0; k + 3 < c; k += 4) {
-                            s0 = fma(-l[k], rowc[k], s0);
-                            s1 = fma(-l[k + 1], rowc[k + 1], s1);
-                            s2 = fma(-l[k + 2], rowc[k + 2], s2);
-                            s3 = fma(-l[k + 3], rowc[k + 3], s3);
+                        const double* rowc = LD + c * PLDL;
+                        double s0 = myrow[c], s1 = 0.0;
+                        int k = 0;
+                        for (; k + 1 < c; k += 2) {
+                            s0 = fma(-myrow[k], rowc[k], s0);
+                            s1 = fma(-myrow[k + 1], rowc[k + 1], s1);
                         }
-#pragma unroll
-                        for (int k = c & ~3; k < c; ++k) s0 = fma(-l[k], rowc[k], s0);
-                        const double sc = (s0 + s1) + (s2 + s3);
+                        if (k < c) s0 = fma(-myrow[k], rowc[k], s0);
+                        const double sc = s0 + s1;
                         const double piv = __shfl_sync(FULL, sc, c);
                         if (!(piv > 0.0)) good = false;
                         const double d = sqrt(piv);
-                        const double inv = 1.0 / d;
-                        l[c] = lane == c ? d : (lane > c ? sc * inv : 0.0);
-                        LD[lane * PLD + c] = l[c];      // row `lane` of L, column c
+                        __syncwarp();
+                        myrow[c] = lane == c ? d : (lane > c ? sc / d : 0.0);
                         __syncwarp();
                     }
-                    // column `lane` of L_dd^-1 by forward substitution: x_r, r >= lane
-                    double x[PNB];
-#pragma unroll
+                    // x = column `lane` of L_dd^-1: x_r = (e_r - sum_{k<r} L(r,k) x_k) / L(r,r)
                     for (int r = 0; r < PNB; ++r) {
-                        const double* rowr = LD + r * PLD;
+                        const double* rowr = LD + r * PLDL;
                         double s0 = (r == lane) ? 1.0 : 0.0, s1 = 0.0;
-#pragma unroll
-                        for (int k = 0; k + 1 < r; k += 2) {
-                            s0 = fma(-rowr[k], x[k], s0);
-                            s1 = fma(-rowr[k + 1], x[k + 1], s1);
+                        int k = lane;                      // x_k = 0 for k < lane
+                        for (; k + 1 < r; k += 2) {
+                            s0 = fma(-rowr[k], LI[k * PLD + lane], s0);
+                            s1 = fma(-rowr[k + 1], LI[(k + 1) * PLD + lane], s1);
                         }
-                        if (r & 1) s0 = fma(-rowr[r - 1], x[r - 1], s0);
-                        x[r] = r < lane ? 0.0 : (s0 + s1) / rowr[r];
+                        if (k < r) s0 = fma(-rowr[k], LI[k * PLD + lane], s0);
+                        LI[r * PLD + lane] = r < lane ? 0.0 : (s0 + s1) / rowr[r];
                     }
-#pragma unroll
-                    for (int r = 0; r < PNB; ++r) LI[r * PLD + lane] = x[r];
                     if (lane == 0) smem[lay.FLAG] = good ? 1.0 : 0.0;
                 }
                 __syncthreads();
@@ -302,18 +318,18 @@ __global__ void __launch_bounds__(PNT, 1) gpr_panel_kernel(VoxelSolveArgs va, Pr
                     break;
                 }
                 // ---- phase B (2): L[j+32:, j:j+32] = P[32:] L_dd^-T (DMMA with L_dd^-1)
-                const int T2 = T - 1;
+                const int T2 = T - PNB / PRT;
                 for (int t = gw; t < T2; t += nw) {
-                    double* src = Pp + (t + 1) * PNB + g;
-                    double fa[4][8];
+                    double* src = Pp + PNB + t * PRT + g;
+                    double fa2[2][8];
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < 2; ++a)
 #pragma unroll
                         for (int kc = 0; kc < 8; ++kc)
-                            fa[a][kc] = __ldcg(src + int64_t(4 * kc + tig) * ldp + 8 * a);
-                    double acc[4][4][2];
+                            fa2[a][kc] = __ldcg(src + int64_t(4 * kc + tig) * ldp + 8 * a);
+                    double acc[2][4][2];
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < 2; ++a)
 #pragma unroll
                         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll
@@ -322,12 +338,12 @@ __global__ void __launch_bounds__(PNT, 1) gpr_panel_kernel(VoxelSolveArgs va, Pr
 #pragma unroll
                         for (int b = 0; b < 4; ++b) fb[b] = LI[(8 * b + g) * PLD + 4 * kc + tig];
 #pragma unroll
-                        for (int a = 0; a < 4; ++a)
+                        for (int a = 0; a < 2; ++a)
 #pragma unroll
-                            for (int b = 0; b < 4; ++b) dmma_acc(acc[a][b][0], acc[a][b][1], fa[a][kc], fb[b]);
+                            for (int b = 0; b < 4; ++b) dmma_acc(acc[a][b][0], acc[a][b][1], fa2[a][kc], fb[b]);
                     }
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < 2; ++a)
 #pragma unroll
                         for (int b = 0; b < 4; ++b)
 #pragma unroll

@@ -342,6 +342,7 @@ class MappingEngine:
                     vm._h(), C.byref(cam), N.ptr(d_image), C.byref(sc), C.byref(out),
                     self.records.count - self.num_gaussians, C.byref(written), N.stream_ptr())
             N.check(rc)
+            vm._log_from_view(int(fi.frame_index), int(fi.ready_transitions), int(di.solved))
             added = int(written.value)
             self.num_gaussians += added
             if self.track_order and added:
@@ -355,6 +356,7 @@ class MappingEngine:
             rc = lib.vx_map_densify(vm._h(), C.byref(di), N.stream_ptr())
             vm._mutated()
             N.check(rc)
+            vm._log_from_view(int(fi.frame_index), int(fi.ready_transitions), int(di.solved))
             if di.first_solves:
                 first, keys = self._first_solves(fi.frame_index)
                 self.pending.append(first)

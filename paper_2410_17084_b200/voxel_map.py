@@ -491,6 +491,29 @@ class VoxelMap:
         idx = torch.as_tensor(np.asarray(vids, dtype=np.int64), device=keys.device)
         return keys.index_select(0, idx).cpu().numpy()
 
+    def _log_from_view(self, frame: int, ready_transitions: int, solved: int):
+        """Event log of a store + densify that ran as one library call
+        (MappingEngine / vx_map_ingest): the frame's UNREADY->READY
+        transitions, then its solves, from the device view."""
+        if not self.record_log:
+            return
+        v = self._view()
+        U = int(v.frame_touched)
+        if ready_transitions and U:
+            vids = N.view_tensor(v.frame_voxels, (U,), np.int32).cpu().numpy()
+            fb = N.view_tensor(v.frame_state_before, (U,), np.uint8).cpu().numpy()
+            fa = N.view_tensor(v.frame_state_after, (U,), np.uint8).cpu().numpy()
+            ch = np.nonzero(fa != fb)[0]
+            self._record_transitions(frame, vids[ch], fb[ch], fa[ch])
+        S = int(v.solve_candidates)
+        if solved and S:
+            st = N.view_tensor(v.solve_status, (S,), np.uint8).cpu().numpy()
+            ok = np.nonzero(st == N.ST_OK)[0]
+            vids = N.view_tensor(v.solve_voxels, (S,), np.int32).cpu().numpy()[ok]
+            bf = N.view_tensor(v.solve_state_before, (S,), np.uint8).cpu().numpy()[ok]
+            af = N.view_tensor(v.solve_state_after, (S,), np.uint8).cpu().numpy()[ok]
+            self._record_solves(frame, vids, bf, af)
+
     def _drain_events(self):
         for kind, frame, keys, a, b in self._events[self._consumed:]:
             for i, k in enumerate(keys.tolist()):

@@ -150,10 +150,20 @@ def test_large_n_panel_kernel_team_sizes(c, monkeypatch):
         f = rng.normal(0, 0.05, n)
         nz = rng.uniform(1e-4, 1e-2, n)
         probs.append(vx.GprProblem(x, f, nz, rng.uniform(0, 0.5, (m, 2)), 4.0))
+    # jitter case: a short kernel (lam 1e4) keeps K + diag(noise) well
+    # conditioned except for one exactly duplicated point with zero noise and the
+    # same target, whose pivot is exactly 0: the plain factorisation must fail
+    # and the +jitter retry succeed, in the oracle as on the device
     x = rng.uniform(0, 0.5, (200, 2))
-    x[17] = x[3]
-    probs.append(vx.GprProblem(x, rng.normal(0, 0.05, 200), np.zeros(200),
-                               rng.uniform(0, 0.5, (81, 2)), 4.0))
+    x[1] = x[0]
+    f = rng.normal(0, 0.05, 200)
+    f[1] = f[0]
+    nz = rng.uniform(1e-4, 1e-2, 200)
+    nz[:2] = 0.0
+    jp = vx.GprProblem(x, f, nz, rng.uniform(0, 0.5, (81, 2)), 1e4)
+    with pytest.raises(Exception):
+        O.posterior(jp.x, jp.f, jp.noise_diag, jp.x_star, jp.lam, jitter=0.0)
+    probs.append(jp)
     batch = vx.gpr_solve_batch(probs)
     assert batch.ok
     for p, r in zip(probs, batch.results):

@@ -1,0 +1,222 @@
+"""GPU: the CUDA path against the round-2 golden fixtures of the reference.
+
+* select_value_axis at its discrete edges (45-degree normals, the 3-axis
+  diagonal, mirror-symmetric sets, lambda_1 at 1e-9 lambda_2): equal to the
+  reference wherever the reference's own decision is not set by rounding
+  noise, and the two device routes (`vx_select_axis_batch`, the densify PCA
+  prepass) agree on every set;
+* the reference's own hot-path unit cases (tests/test_gpr.py:17-88,
+  test_voxel_map.py:143-154, test_acceptance.py c04, c05, c10);
+* a 4-frame `MappingPipeline.ingest_frame` replay with a deferred expansion
+  threshold through `MappingEngine(expansion_threshold=400)`;
+* the stream directory the reference wrote, read by `read_stream` and
+  ingested straight from the PLY records by `stream_frames` + `ingest_stream`.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2410_17084_b200 as vx
+from tests import _fixtures as F
+from tests.test_golden_r2 import axis_edge_sets, axis_margin
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-9, 1e-12
+POS_ATOL = 1e-11
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2410_17084_b200 import _native as N
+    N.lib()
+
+
+def _densify_axis(pts):
+    """Axis chosen by the densify path (PCA prepass) for one point set."""
+    vmap = vx.VoxelMap(1.0, 1e-4, tau=3, eta=0.3)
+    lo = np.floor(pts.min(axis=0))
+    p = pts - lo + 0.25 * 0           # keep the set inside one unit voxel
+    assert np.all(np.floor(p) == np.floor(p[0]))
+    u = vmap.store_frame(vx.PointCloud(p, np.full((len(p), 3), 0.5), np.zeros(len(p))))
+    preds = vx.densify_frame(u, vmap, vx.PipelineConfig(voxel_size=1.0, tau=3))
+    cell = next(iter(vmap.cells.values()))
+    return cell.value_axis if preds else -1
+
+
+def test_axis_edges_match_reference_and_routes_agree():
+    sets = axis_edge_sets()
+    decided = unresolved = 0
+    for i, (pts, ax, kind, ev, nrm) in enumerate(sets):
+        try:
+            a = vx.select_value_axis(pts).value_axis
+        except vx.DegenerateGeometryError:
+            a = -1
+        tie, deg = axis_margin(ev, nrm)
+        # the reference's decision is a rounding outcome when the two largest
+        # |normal| components (or lambda_1 and 1e-9 lambda_2) agree to ~1e-12
+        if tie > 1e-12 and deg > 1e-12:
+            assert a == ax, (i, kind, ax, a, tie, deg)
+            decided += 1
+        else:
+            unresolved += 1
+        # both device routes run the same covariance + eigensolver code
+        assert _densify_axis(pts) == a, (i, kind)
+    assert decided >= 90
+    print(f"axis edges: {decided} decided cases equal to the reference, "
+          f"{unresolved} rounding-level ties")
+
+
+def test_reference_plane_and_relabelling_cases():
+    d = F.load("unit_cases.npz")
+    for k in ("horizontal", "vertical", "slanted"):
+        assert vx.select_value_axis(d[k]).value_axis == int(d[k + "_axis"])
+    pts = d["relabel_pts"]
+    sel, sel_p = vx.select_value_axis(pts), vx.select_value_axis(pts[:, [2, 0, 1]])
+    assert (sel.value_axis, sel_p.value_axis) == tuple(d["relabel_axes"])
+    grid = vx.make_mesh_grid(((0, 0.2), (0, 0.2)), 2, 2)
+    noise = np.full(len(pts), 1e-4)
+    r = vx.gpr_solve(vx.GprProblem(sel.x, sel.f - sel.f.mean(), noise, grid))
+    r_p = vx.gpr_solve(vx.GprProblem(sel_p.x, sel_p.f - sel_p.f.mean(), noise, grid))
+    out = vx.gpr.assemble_points(2, grid, r.mu_star + sel.f.mean())
+    out_p = vx.gpr.assemble_points(0, grid, r_p.mu_star + sel_p.f.mean())
+    np.testing.assert_allclose(out_p, out[:, [2, 0, 1]], atol=1e-9)   # test_gpr.py:88
+    np.testing.assert_allclose(out, d["relabel_out"], rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(out_p, d["relabel_out_p"], rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(r.sigma_star_diag, d["relabel_var"], rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(r_p.sigma_star_diag, d["relabel_var_p"], rtol=RTOL, atol=ATOL)
+
+
+def test_reference_c04_and_successive_solves():
+    d = F.load("unit_cases.npz")
+    config = vx.PipelineConfig(sensor_var=0.25, kernel_lambda=40.0, eta=0.3, tau=10)
+    vmap = vx.VoxelMap.from_config(config)
+    keys = [vx.VoxelKey(*k) for k in d["c04_keys"].tolist()]
+    for fr, pts in enumerate(d["c04_frames"]):
+        u = vmap.store_frame(vx.PointCloud(pts, np.full((len(pts), 3), 0.5), np.zeros(len(pts))))
+        vx.densify_frame(u, vmap, config)
+        hist = [vmap.cells[k].mean_posterior_variance if vmap.cells[k].solved else np.nan
+                for k in keys]
+        np.testing.assert_allclose(hist, d["c04_hist"][fr], rtol=RTOL, atol=ATOL)
+    h = d["c04_hist"]
+    assert np.all(np.diff(h, axis=0)[~np.isnan(np.diff(h, axis=0))] <= 1e-9)
+    assert [int(vmap.cells[k].state) for k in keys] == d["c04_states"].tolist()
+    config = vx.PipelineConfig(sensor_var=0.25, kernel_lambda=40.0, eta=1e-6)
+    vmap = vx.VoxelMap.from_config(config)
+    means = []
+    for pts in d["succ_clouds"]:
+        u = vmap.store_frame(vx.PointCloud(pts, np.full((len(pts), 3), 0.5), np.zeros(len(pts))))
+        vx.densify_frame(u, vmap, config)
+        means.append(vmap.cell(vx.VoxelKey(0, 0, 0)).mean_posterior_variance)
+    np.testing.assert_allclose(means, d["succ_means"], rtol=RTOL, atol=ATOL)
+    assert means[1] <= means[0] + 1e-9
+
+
+def test_reference_c05_densification_accuracy():
+    d = F.load("unit_cases.npz")
+    config = vx.PipelineConfig(sensor_var=1e-4)
+    vmap = vx.VoxelMap.from_config(config)
+    pos = d["c05_positions"]
+    preds = vx.densify_frame(vmap.store_frame(vx.PointCloud(pos, d["c05_colors"], np.zeros(len(pos)))),
+                             vmap, config)
+    np.testing.assert_array_equal(np.array([p.key for p in preds]), d["c05_pred_keys"])
+    got = np.stack([p.positions for p in preds])
+    np.testing.assert_allclose(got, d["c05_pred_positions"], rtol=0, atol=POS_ATOL)
+    np.testing.assert_allclose(np.stack([p.variances for p in preds]), d["c05_pred_variances"],
+                               rtol=RTOL, atol=ATOL)
+    n, off = d["c05_plane"][:3], d["c05_plane"][3]
+    dist = got.reshape(-1, 3) @ (n / np.linalg.norm(n)) - off
+    assert all(len(p) == 81 for p in preds)
+    assert np.sqrt(np.mean(dist ** 2)) <= 0.02          # test_acceptance.py:172
+
+
+def test_reference_c10_batch_and_determinism():
+    d = F.load("unit_cases.npz")
+    ox = np.concatenate([[0], np.cumsum(d["c10_n"])])
+    oq = np.concatenate([[0], np.cumsum(d["c10_m"])])
+    probs = [vx.GprProblem(d["c10_x"][ox[i]:ox[i + 1]], d["c10_f"][ox[i]:ox[i + 1]],
+                           d["c10_noise"][ox[i]:ox[i + 1]], d["c10_xs"][oq[i]:oq[i + 1]],
+                           float(d["c10_lam"][i])) for i in range(len(d["c10_n"]))]
+    a, b = vx.gpr_solve_batch(probs, workers=4), vx.gpr_solve_batch(probs)
+    assert a.ok and b.ok
+    for i, (ra, rb) in enumerate(zip(a.results, b.results)):
+        np.testing.assert_array_equal(ra.mu_star, rb.mu_star)            # bit-identical reruns
+        np.testing.assert_array_equal(ra.sigma_star_diag, rb.sigma_star_diag)
+        single = vx.gpr_solve(probs[i])
+        np.testing.assert_allclose(single.mu_star, ra.mu_star, atol=1e-12)   # c10: 1e-12
+        np.testing.assert_allclose(ra.mu_star, d["c10_mu"][oq[i]:oq[i + 1]], rtol=RTOL, atol=ATOL)
+        np.testing.assert_allclose(ra.sigma_star_diag, d["c10_var"][oq[i]:oq[i + 1]],
+                                   rtol=RTOL, atol=ATOL)
+
+
+def test_engine_expansion_threshold_matches_reference_replay(tmp_path):
+    d = F.load("scan_threshold.npz")
+    vs, eta, sv, tau, thr = d["config"]
+    config = vx.PipelineConfig(voxel_size=float(vs), eta=float(eta), sensor_var=float(sv),
+                               tau=int(tau), expansion_threshold=int(thr), iterations=0)
+    eng = vx.MappingEngine(config)
+    first = 0
+    for fr in range(4):
+        p = f"f{fr}_"
+        cam = vx.Camera(60.0, 60.0, 39.5, 29.5, 80, 60, d[p + "R"], d[p + "t"])
+        rep = eng.ingest(d[p + "positions"], d[p + "colors"], cam, d[p + "image"])
+        want = d[p + "report"]
+        assert [rep.voxels_touched, rep.voxels_solved, rep.newly_active,
+                rep.primitives_added] == [want[0], want[1], want[2], want[4]]
+        assert eng._pending_n == int(d[p + "pending"])
+        g = {k: v[first:].cpu().numpy() for k, v in eng.gaussians_device().items()}
+        first = eng.num_gaussians
+        np.testing.assert_array_equal(g["source_key"], d[p + "g_source_keys"])
+        # Gaussians are 1/sigma^2-weighted moments of the predictions: they
+        # inherit the variances' 1e-9 relative agreement (test_full_size.py)
+        np.testing.assert_allclose(g["position"], d[p + "g_positions"], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(g["scale"], d[p + "g_scales"], rtol=1e-8, atol=1e-12)
+        np.testing.assert_allclose(g["color"], d[p + "g_colors"], rtol=0, atol=1e-9)
+        np.testing.assert_array_equal(g["rotation"], d[p + "g_rotations"])
+        np.testing.assert_array_equal(g["opacity"], d[p + "g_opacities"])
+    # the map file: same header and config echo bytes as the reference's
+    out = tmp_path / "ours.map"
+    vx.formats.write_map(out, eng, config)
+    ours, ref = out.read_bytes(), open(os.path.join(F.GOLDEN, "map_ref.map"), "rb").read()
+    assert len(ours) == len(ref)
+    hdr = 8 + 16 + int(np.frombuffer(ref[20:24], dtype="<u4")[0])
+    assert ours[:hdr] == ref[:hdr]
+    gm, _ = vx.formats.read_map(out)
+    gr, _ = vx.formats.read_map(os.path.join(F.GOLDEN, "map_ref.map"))
+    np.testing.assert_allclose(gm.positions, gr.positions, rtol=0, atol=1e-9)
+    np.testing.assert_array_equal(gm.source_keys, gr.source_keys)
+
+
+def test_read_stream_matches_reference():
+    d = F.load("stream_ref.npz")
+    frames = vx.stream.read_stream(os.path.join(F.GOLDEN, "stream"))
+    assert len(frames) == 3
+    for i, f in enumerate(frames):
+        p = f"f{i}_"
+        assert f.timestamp == float(d[p + "ts"])
+        np.testing.assert_array_equal(f.points.positions, d[p + "positions"])
+        np.testing.assert_array_equal(f.points.colors, d[p + "colors"])
+        np.testing.assert_array_equal(f.image, d[p + "image"])
+        np.testing.assert_array_equal(f.camera.rotation, d[p + "R"])
+        np.testing.assert_array_equal(f.camera.translation, d[p + "t"])
+
+
+def test_stream_frames_ingest_equals_host_ingest():
+    """PLY records H2D + device decode inside ingest_stream == host read_stream + ingest."""
+    sdir = os.path.join(F.GOLDEN, "stream")
+    config = vx.PipelineConfig(voxel_size=0.2)
+    a = vx.MappingEngine(config)
+    ra = a.ingest_stream(vx.stream.stream_frames(sdir))
+    b = vx.MappingEngine(config)
+    rb = [b.ingest(f.points.positions, f.points.colors, f.camera, f.image)
+          for f in vx.stream.read_stream(sdir)]
+    assert [r.voxels_solved for r in ra] == [r.voxels_solved for r in rb]
+    assert sum(r.primitives_added for r in ra) > 0
+    ga, gb = a.gaussians_device(), b.gaussians_device()
+    for k in gb:
+        assert ga[k].shape == gb[k].shape and bool((ga[k] == gb[k]).all()), k
