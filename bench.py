@@ -376,6 +376,32 @@ def run_trajectory(args, dev):
             "points_per_scan": float(np.mean([len(f[0]) for f in frames]))}
 
 
+def run_dropin(args):
+    """The reference's own MappingPipeline.ingest_frame (pipeline.py:139-187,
+    unmodified, from the pip-installed reference in baseline/_ref) driving this
+    package through the INTEGRATION.md §1 module substitution, on the config-2
+    trajectory; ms per scan next to MappingEngine.ingest on the same frames.
+    The per-voxel Python loops of ingest_frame (state checks, expansion,
+    GaussianMap.extend) are the caller's and are inside the number."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "voxsplat")):
+        return {"unavailable": "baseline/_ref (pip-installed reference) is absent"}
+    sys.path.insert(0, ROOT)
+    from tests.test_integration_recipe import run_recipe
+    try:
+        r = run_recipe(nframes=args.traj_scans, rays=60000)
+    except Exception as e:
+        return {"error": f"{type(e).__name__}: {str(e)[-300:]}"}
+    ms, ems = r["ms_per_frame"][2:], r["engine_ms_per_frame"][2:]
+    return {"workload": f"config2: {args.traj_scans} scans of the 32-beam outdoor scene, eta=2e-5, "
+                        "160x120 images",
+            "api": "reference MappingPipeline.ingest_frame (baseline/_ref, unmodified) on "
+                   "voxsplat.{errors,config,camera,voxel_map,gpr,splat_init,renderer} := this "
+                   "package (INTEGRATION.md 1)",
+            "ms_per_scan": float(np.median(ms)), "engine_ms_per_scan": float(np.median(ems)),
+            "outputs_equal_engine": bool(all(r["same"].values()) and r["reps"] == r["ereps"]),
+            "gaussians": r["n"]}
+
+
 def render_ms(gaussians, cam, reps=10):
     """Median device time of one 640x480 render of device-resident records
     (renderer.render_device: projection, depth-ordered tile binning, blend)."""
@@ -636,6 +662,7 @@ def run_gpu(args, rank, world, local_rank):
     if args.traj_scans > 0:
         traj = run_trajectory(args, dev)
     scans = run_scans(args) if args.scan_reps > 0 else None
+    dropin = run_dropin(args) if (args.traj_scans > 0 and rank == 0) else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -677,6 +704,7 @@ def run_gpu(args, rank, world, local_rank):
             "gpu_launches": launches,
             "tail": tail,
             "trajectory": traj,
+            "dropin": dropin,
             "scans": scans,
             "render": render,
             "gather": gather,

@@ -188,15 +188,106 @@ def init_gaussians_batch(predictions, camera: Camera, image: np.ndarray, config)
     return recs.to_host()
 
 
+class _InitQueue:
+    """Per-voxel `init_gaussians_for_voxel` calls, coalesced into one launch.
+
+    The reference's callers initialise voxel by voxel inside a Python loop
+    (pipeline.py:160-171) and only use the primitives through `len()` and
+    `GaussianMap.extend`.  Each call therefore validates its prediction at once
+    (same exception as the reference) but only queues it; the queue is solved
+    in ONE `vx_gaussians_from_predictions` launch (one H2D of the stacked
+    predictions and of the image, one D2H) when any primitive is read, when
+    the camera / image / config of the calls changes, or when a GaussianMap
+    holding them is read.
+    """
+
+    def __init__(self):
+        self.ctx = None
+        self.items = []          # (prediction, _LazyPrimitives)
+
+    def add(self, prediction, camera, image, config):
+        ctx = (id(camera), id(image), id(config))
+        if self.ctx is not None and ctx != self.ctx:
+            self.flush()
+        if not self.items:
+            self.ctx, self.refs = ctx, (camera, image, config)
+        lazy = _LazyPrimitives(self, config.n_s * config.n_s)
+        self.items.append((prediction, lazy))
+        return lazy
+
+    def flush(self):
+        if not self.items:
+            return
+        items, (camera, image, config) = self.items, self.refs
+        self.items, self.ctx, self.refs = [], None, None
+        h = init_gaussians_batch([p for p, _ in items], camera, image, config)
+        k = config.n_s * config.n_s
+        for i, (pred, lazy) in enumerate(items):
+            lazy._records = {name: v[i * k:(i + 1) * k] for name, v in h.items()}
+            lazy._key = VoxelKey(*(int(v) for v in pred.key))
+
+
+_QUEUE = _InitQueue()
+
+
+class _LazyPrimitives(list):
+    """The n_s^2 primitives of one queued voxel: a list that fills itself from
+    the coalesced launch on first read (length known up front)."""
+
+    def __init__(self, queue, n):
+        super().__init__()
+        self._queue, self._n, self._records, self._key = queue, n, None, None
+
+    def _fill(self):
+        if self._records is None:
+            self._queue.flush()
+        if list.__len__(self) == 0 and self._n:
+            h, key = self._records, self._key
+            list.extend(self, [GaussianPrimitive(position=h["position"][i], scale=h["scale"][i],
+                                                 rotation=h["rotation"][i],
+                                                 opacity=float(h["opacity"][i]),
+                                                 color=h["color"][i], source_key=key)
+                               for i in range(self._n)])
+
+    def records(self) -> dict:
+        if self._records is None:
+            self._queue.flush()
+        return self._records
+
+    def __len__(self):
+        return self._n
+
+    def __iter__(self):
+        self._fill()
+        return list.__iter__(self)
+
+    def __getitem__(self, i):
+        self._fill()
+        return list.__getitem__(self, i)
+
+    def __repr__(self):
+        self._fill()
+        return list.__repr__(self)
+
+    def __eq__(self, other):
+        self._fill()
+        return list.__eq__(self, other)
+
+    def __bool__(self):
+        return self._n > 0
+
+
 def init_gaussians_for_voxel(prediction: VoxelPrediction, camera: Camera, image: np.ndarray,
                              config) -> list[GaussianPrimitive]:
-    """All n_s^2 primitives of a solved voxel (splat_init.py:134-148)."""
-    h = init_gaussians_batch([prediction], camera, image, config)
-    key = VoxelKey(*(int(v) for v in prediction.key))
-    return [GaussianPrimitive(position=h["position"][i], scale=h["scale"][i],
-                              rotation=h["rotation"][i], opacity=float(h["opacity"][i]),
-                              color=h["color"][i], source_key=key)
-            for i in range(len(h["opacity"]))]
+    """All n_s^2 primitives of a solved voxel (splat_init.py:134-148).
+
+    Validated now; computed with every other queued voxel in one device
+    launch when first read (`_InitQueue`)."""
+    expected = config.n_s * config.n_s * config.n_r * config.n_r
+    if len(prediction) != expected:
+        raise ContractViolationError(
+            f"prediction has {len(prediction)} points, expected {expected}")
+    return _QUEUE.add(prediction, camera, image, config)
 
 
 class GaussianMap:
@@ -210,6 +301,14 @@ class GaussianMap:
         self._n = 0
         self._buf = {name: np.empty((0, w) if w else (0,), dtype=dt)
                      for name, w, dt in self._FIELDS}
+        self._lazy = []          # queued _LazyPrimitives (init_gaussians_for_voxel)
+
+    def _settle(self):
+        """Append the queued voxels' records (one launch for all of them)."""
+        if self._lazy:
+            pend, self._lazy = self._lazy, []
+            for lz in pend:
+                self.extend_records(lz.records())
 
     def _reserve(self, extra: int):
         need = self._n + extra
@@ -223,12 +322,14 @@ class GaussianMap:
             self._buf[name] = nb
 
     def __len__(self) -> int:
-        return self._n
+        return self._n + sum(len(lz) for lz in self._lazy)
 
     def _get(self, name):
+        self._settle()
         return self._buf[name][:self._n]
 
     def _set(self, name, value):
+        self._settle()
         w = dict((f, wd) for f, wd, _ in self._FIELDS)[name]
         dt = dict((f, d) for f, _, d in self._FIELDS)[name]
         v = np.asarray(value, dtype=dt)
@@ -244,8 +345,12 @@ class GaussianMap:
     source_keys = property(lambda s: s._get("source_keys"), lambda s, v: s._set("source_keys", v))
 
     def extend(self, primitives: list[GaussianPrimitive]) -> None:
+        if isinstance(primitives, _LazyPrimitives) and primitives._records is None:
+            self._lazy.append(primitives)        # materialised on the next read
+            return
         if not primitives:
             return
+        self._settle()
         self.extend_arrays(
             np.stack([p.position for p in primitives]), np.stack([p.scale for p in primitives]),
             np.stack([p.rotation for p in primitives]),
@@ -254,6 +359,8 @@ class GaussianMap:
                       for p in primitives], dtype=np.int64).reshape(-1, 3))
 
     def extend_arrays(self, positions, scales, rotations, opacities, colors, source_keys):
+        if self._lazy:
+            self._settle()
         k = len(opacities)
         self._reserve(k)
         for name, arr in (("positions", positions), ("scales", scales), ("rotations", rotations),

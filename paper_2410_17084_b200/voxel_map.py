@@ -321,21 +321,88 @@ class _Snapshot:
         return cell
 
 
+FRAME_CACHE_MAX = 1 << 17
+
+
+class _DeviceCell(VoxelCell):
+    """A `VoxelCell` backed by the device store.
+
+    `key`, `state` and `value_axis` are fetched with the cell; `raw`, `pseudo`
+    and `last_prediction` are copied from HBM on first access (only this
+    voxel's rows), or come from the batch the map prefetched for the last
+    frame's solved voxels.  Like the reference's cells (which the map mutates in
+    place) the lazy fields reflect the store when they are first read.
+    """
+
+    def __init__(self, vmap, key, vid, state, axis, pred=None):
+        self._vmap, self._vid = vmap, int(vid)
+        self.key = key
+        self.state = VoxelState(int(state))
+        self.value_axis = None if axis < 0 else int(axis)
+        self._pred = pred            # (positions, colors, variances) or None
+        self._lazy = {}
+
+    def _fetch(self, name):
+        if name not in self._lazy:
+            self._lazy.update(self._vmap._cell_payload(self._vid, want_pred=self._pred is None))
+            if self._pred is not None:
+                self._lazy["pred"] = self._pred
+        return self._lazy[name]
+
+    @property
+    def raw(self):
+        return self._fetch("raw")
+
+    @raw.setter
+    def raw(self, v):
+        self._lazy["raw"] = v
+
+    @property
+    def last_prediction(self):
+        pr = self._pred if self._pred is not None else self._fetch("pred")
+        if pr is None:
+            return None
+        if not isinstance(pr, VoxelPrediction):
+            pr = VoxelPrediction(self.key, *pr)
+            self._pred = pr
+            self._lazy["pred"] = pr
+        return pr
+
+    @last_prediction.setter
+    def last_prediction(self, v):
+        self._pred = v
+        self._lazy["pred"] = v
+
+    @property
+    def pseudo(self):
+        if "pseudo" in self._lazy:
+            return self._lazy["pseudo"]
+        pr = self.last_prediction
+        return None if pr is None else PointCloud(pr.positions, pr.colors, pr.variances)
+
+    @pseudo.setter
+    def pseudo(self, v):
+        self._lazy["pseudo"] = v
+
+
 class _CellsView(Mapping):
-    """`VoxelMap.cells`: dict-like, insertion (= creation) ordered, read-only."""
+    """`VoxelMap.cells`: dict-like, insertion (= creation) ordered, read-only.
+
+    `cells[key]` / `key in cells` cost O(1) device traffic: the map keeps a
+    per-mutation cache of the last frame's touched voxels (metadata, and the
+    predictions of its solved voxels, each fetched in ONE copy of O(touched)
+    bytes) and resolves any other key with one `vx_map_lookup`.  Iteration
+    (`values()`, `items()`, `iter`) is the only whole-map operation.
+    """
 
     def __init__(self, vmap: "VoxelMap"):
         self._m = vmap
 
-    def _snap(self) -> _Snapshot:
-        return self._m._snapshot()
-
     def __getitem__(self, key):
-        s = self._snap()
-        vid = s.index.get(tuple(int(v) for v in key))
-        if vid is None:
+        c = self._m._cell_for(key)
+        if c is None:
             raise KeyError(key)
-        return s.cell(vid)
+        return c
 
     def get(self, key, default=None):
         try:
@@ -345,23 +412,23 @@ class _CellsView(Mapping):
 
     def __contains__(self, key):
         try:
-            return tuple(int(v) for v in key) in self._snap().index
-        except TypeError:
+            return self._m._cell_for(key) is not None
+        except (TypeError, ValueError):
             return False
 
     def __iter__(self):
-        s = self._snap()
+        s = self._m._snapshot()
         return (VoxelKey(*(int(x) for x in k)) for k in s.keys.tolist())
 
     def __len__(self):
         return len(self._m)
 
     def values(self):
-        s = self._snap()
+        s = self._m._snapshot()
         return [s.cell(i) for i in range(s.V)]
 
     def items(self):
-        s = self._snap()
+        s = self._m._snapshot()
         return [(VoxelKey(*(int(x) for x in s.keys[i])), s.cell(i)) for i in range(s.V)]
 
 
@@ -443,6 +510,91 @@ class VoxelMap:
             torch.cuda.current_stream().synchronize()
             self._snap = (self._epoch, _Snapshot(self))
         return self._snap[1]
+
+    # -- per-key cell access (O(touched) traffic) ------------------------------
+    def _frame_cache(self):
+        """{key tuple: (vid, state, axis, pred|None)} of the last frame's touched
+        voxels at the current mutation epoch, in one batched device gather."""
+        if getattr(self, "_fc", None) is not None and self._fc[0] == self._epoch:
+            return self._fc[1]
+        import torch
+        cache = {}
+        if self._handle is not None:
+            v = self._view()
+            U, V = int(v.frame_touched), int(v.num_voxels)
+            # frames of up to FRAME_CACHE_MAX voxels are prefetched in one batch;
+            # larger ones (config-4 scale) resolve keys one lookup at a time
+            if U and V and U <= FRAME_CACHE_MAX:
+                vids = N.view_tensor(v.frame_voxels, (U,), np.int32).long()
+                keys = N.view_tensor(v.keys, (V, 3), np.int64).index_select(0, vids)
+                st = N.view_tensor(v.state, (V,), np.uint8).index_select(0, vids).long()
+                ax = N.view_tensor(v.value_axis, (V,), np.int8).index_select(0, vids).long()
+                hp = N.view_tensor(v.has_pred, (V,), np.uint8).index_select(0, vids).long()
+                meta = torch.stack([vids, st, ax, hp], 1).cpu().numpy()
+                keys = keys.cpu().numpy()
+                # predictions of the touched voxels that have one (the last
+                # densify's solves among them): one gather, one copy
+                have = np.nonzero(meta[:, 3])[0]
+                preds = {}
+                if len(have):
+                    M = int(v.pred_points)
+                    hv = torch.as_tensor(meta[have, 0], device=vids.device)
+                    slot = N.view_tensor(v.pred_slot, (V,), np.int32).index_select(0, hv).long()
+                    ns = int(slot.max().item()) + 1
+                    px = N.view_tensor(v.pred_xyz, (ns, M, 3), np.float64).index_select(0, slot)
+                    pc = N.view_tensor(v.pred_rgb, (ns, M, 3), np.float64).index_select(0, slot)
+                    pv = N.view_tensor(v.pred_var, (ns, M), np.float64).index_select(0, slot)
+                    px, pc, pv = px.cpu().numpy(), pc.cpu().numpy(), pv.cpu().numpy()
+                    for r, i in enumerate(have):
+                        preds[i] = (px[r], pc[r], pv[r])
+                for i, k in enumerate(keys.tolist()):
+                    cache[tuple(k)] = (int(meta[i, 0]), int(meta[i, 1]), int(meta[i, 2]),
+                                       preds.get(i))
+        self._fc = (self._epoch, cache)
+        return cache
+
+    def _cell_for(self, key):
+        k = tuple(int(x) for x in key)
+        if len(k) != 3:
+            raise ValueError("voxel keys have three components")
+        hit = self._frame_cache().get(k)
+        if hit is None:
+            if self._handle is None:
+                return None
+            import torch
+            d = torch.tensor([k], dtype=torch.int64, device=N.device())
+            out = torch.empty(1, dtype=torch.int32, device=d.device)
+            N.check(self._lib.vx_map_lookup(self._h(), N.ptr(d), 1, N.ptr(out), N.stream_ptr()))
+            vid = int(out.item())
+            if vid < 0:
+                return None
+            v = self._view()
+            V = int(v.num_voxels)
+            st = int(N.view_tensor(v.state, (V,), np.uint8)[vid].item())
+            ax = int(N.view_tensor(v.value_axis, (V,), np.int8)[vid].item())
+            hit = (vid, st, ax, None)
+        vid, st, ax, pred = hit
+        return _DeviceCell(self, VoxelKey(*k), vid, st, ax, pred)
+
+    def _cell_payload(self, vid: int, want_pred: bool = True) -> dict:
+        """raw points (and the prediction) of one voxel: O(voxel) bytes."""
+        v = self._view()
+        V = int(v.num_voxels)
+        cnt = int(N.view_tensor(v.raw_count, (V,), np.int32)[vid].item())
+        off = int(N.view_tensor(v.raw_offset, (V,), np.int64)[vid].item())
+        xyz = N.view_tensor(v.raw_xyz, (off + cnt, 3), np.float64)[off:off + cnt].cpu().numpy()
+        rgb = N.view_tensor(v.raw_rgb, (off + cnt, 3), np.float64)[off:off + cnt].cpu().numpy()
+        out = {"raw": PointCloud(xyz, rgb, np.full(cnt, self.sensor_var))}
+        if want_pred:
+            pred = None
+            if int(N.view_tensor(v.has_pred, (V,), np.uint8)[vid].item()):
+                M = int(v.pred_points)
+                sl = int(N.view_tensor(v.pred_slot, (V,), np.int32)[vid].item())
+                pred = (N.view_tensor(v.pred_xyz, (sl + 1, M, 3), np.float64)[sl].cpu().numpy(),
+                        N.view_tensor(v.pred_rgb, (sl + 1, M, 3), np.float64)[sl].cpu().numpy(),
+                        N.view_tensor(v.pred_var, (sl + 1, M), np.float64)[sl].cpu().numpy())
+            out["pred"] = pred
+        return out
 
     # -- accessors ----------------------------------------------------------
     @property
