@@ -44,7 +44,7 @@ namespace vx {
 // read back (and reset) by the extra export vx_phase_cycles
 // (tools/phase_timing.py).  Compiled out otherwise.
 #ifdef VX_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[12];
+__device__ unsigned long long g_phase_cycles[20];
 #define VX_PHASE(id, t0)                                                                  \
     do {                                                                                  \
         if (threadIdx.x == 0) {                                                           \
@@ -2716,10 +2716,12 @@ static int panel_team_size(int num_items) {
         const int c = atoi(e);
         if (c == 1 || c == 2 || c == 4 || c == 8) return c;
     }
+    // up to two rounds of the team count: the largest voxel (first in the
+    // queue) sets the latency, so bigger teams win (config 3: ~30 items)
     const int sms = sm_count();
-    if (num_items * 8 <= sms) return 8;
-    if (num_items * 4 <= sms) return 4;
-    if (num_items * 2 <= sms) return 2;
+    if (num_items * 4 <= sms) return 8;
+    if (num_items * 2 <= sms) return 4;
+    if (num_items <= sms) return 2;
     return 1;
 }
 
@@ -3002,11 +3004,11 @@ int launch_problem_solve(const VxGprBatch& b, const int32_t* d_items, int32_t co
 #ifdef VX_PHASE_TIMING
 // diagnostics-build export: copy out and reset the per-phase cycle sums
 extern "C" int vx_phase_cycles(unsigned long long* out, int max_phases) {
-    unsigned long long h[12];
+    unsigned long long h[20];
     if (cudaMemcpyFromSymbol(h, vx::g_phase_cycles, sizeof(h)) != cudaSuccess) return -1;
-    const unsigned long long z[12] = {};
+    const unsigned long long z[20] = {};
     cudaMemcpyToSymbol(vx::g_phase_cycles, z, sizeof(z));
-    const int k = max_phases < 12 ? max_phases : 12;
+    const int k = max_phases < 20 ? max_phases : 20;
     for (int i = 0; i < k; ++i) out[i] = h[i];
     return k;
 }

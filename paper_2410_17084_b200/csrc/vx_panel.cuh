@@ -59,7 +59,7 @@ __host__ __device__ inline int64_t panel_base(int R, int p) {
 }
 
 struct PanelLayout {
-    int X, F, NZ, GC, QT, LD, LI, MU, VAR, COL, FLAG, total;
+    int X, F, NZ, GC, QT, LD, LI, BS, DINV, MU, VAR, COL, FLAG, total;
     __host__ __device__ PanelLayout(int np32, int mcols, int mmax) {
         int o = 0;
         X = o; o += 2 * np32;
@@ -69,6 +69,9 @@ struct PanelLayout {
         QT = o; o += mcols / 2 + 1;       // int32 (ri | si << 16) per column
         LD = o; o += PNB * PLD;           // factored diagonal block (row-major)
         LI = o; o += PNB * PLD;           // its inverse (row-major)
+        o = (o + 1) & ~1;                 // 16-byte aligned for cp.async
+        BS = o; o += 2 * PNB * PLD;       // phase-A B operand blocks (double buffer)
+        DINV = o; o += PNB;               // 1 / L_dd(r, r)
         MU = o; o += mcols;
         VAR = o; o += mcols;
         COL = o; o += 3 * mmax + 1;
@@ -86,10 +89,168 @@ __device__ __forceinline__ void team_sync(int csize) {
     }
 }
 
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ unsigned cluster_rank() {
     unsigned r;
     asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
+}
+
+// Cholesky factor L_dd and its inverse of the 32x32 diagonal block of a panel,
+// by one warp (every CTA of the team runs it redundantly on the same data, so
+// all take the same pivot decision).  In: the block P at panel storage `P`
+// (column-major, ld `ldp`, lower part used).  Out: LD = L_dd (row-major,
+// stride PLDL, lower), LI = L_dd^-1 (row-major, stride PLD, zeros above the
+// diagonal), DINV[r] = 1 / L_dd(r, r); returns false when a pivot is not > 0
+// (dpotrf's failure rule, gpr.py:187-192).
+//
+// Blocked right-looking by 8 columns: every lane factors the 8x8 diagonal
+// block in its own registers (dpotf2 order: pivot p, l = 1/sqrt(p) scaling,
+// rank-1 update; the reciprocal square root is the only transcendental and
+// there is no division), the lanes of the rows below solve their row against
+// it and apply the block's rank-8 update to the rest of their row.  L_dd^-1:
+// lane (block, column) forms column `column` of the 8x8 block inverse, then the
+// off-diagonal blocks by block diagonal, L^-1_ij = -D^-1_i sum_k L_ik L^-1_kj.
+__device__ __noinline__ bool diag_block_factor(const double* __restrict__ P, int ldp, double* LD,
+                                               double* LI, double* DINV, int lane) {
+#pragma unroll 4
+    for (int c = 0; c < PNB; ++c) LD[lane * PLDL + c] = __ldcg(P + int64_t(c) * ldp + lane);
+    __syncwarp();
+    bool good = true;
+#pragma unroll 1
+    for (int kb = 0; kb < 4; ++kb) {
+        const int b0 = 8 * kb;
+        double a[36];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c <= r; ++c) a[r * (r + 1) / 2 + c] = LD[(b0 + r) * PLDL + b0 + c];
+        double inv[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const double piv = a[c * (c + 1) / 2 + c];
+            if (!(piv > 0.0)) good = false;
+            inv[c] = rsqrt(piv);
+            a[c * (c + 1) / 2 + c] = piv * inv[c];
+#pragma unroll
+            for (int r = c + 1; r < 8; ++r) a[r * (r + 1) / 2 + c] *= inv[c];
+#pragma unroll
+            for (int r = c + 1; r < 8; ++r)
+#pragma unroll
+                for (int k = c + 1; k <= r; ++k)
+                    a[r * (r + 1) / 2 + k] = fma(-a[r * (r + 1) / 2 + c], a[k * (k + 1) / 2 + c],
+                                                 a[r * (r + 1) / 2 + k]);
+        }
+        __syncwarp();
+        // the block's own rows (lane in [b0, b0 + 8)) and 1/L_rr
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            if (lane == b0 + r) {
+#pragma unroll
+                for (int c = 0; c <= r; ++c) LD[lane * PLDL + b0 + c] = a[r * (r + 1) / 2 + c];
+                DINV[lane] = inv[r];
+            }
+        if (kb < 3) {
+            const bool below = lane >= b0 + 8;
+            double v[8];
+            if (below) {
+                double* row = LD + lane * PLDL + b0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) v[c] = row[c];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    v[c] *= inv[c];
+#pragma unroll
+                    for (int k = c + 1; k < 8; ++k) v[k] = fma(-v[c], a[k * (k + 1) / 2 + c], v[k]);
+                }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) row[c] = v[c];
+            }
+            __syncwarp();
+            // rank-8 update of the rest of the row: LD[r][k] -= sum_i L[r][b0+i] L[k][b0+i]
+            if (below) {
+                double* row = LD + lane * PLDL;
+                int k = b0 + 8;
+                for (; k + 1 <= lane; k += 2) {
+                    const double* l0 = LD + k * PLDL + b0;
+                    const double* l1 = l0 + PLDL;
+                    double s0 = row[k], s1 = row[k + 1];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        s0 = fma(-v[i], l0[i], s0);
+                        s1 = fma(-v[i], l1[i], s1);
+                    }
+                    row[k] = s0;
+                    row[k + 1] = s1;
+                }
+                if (k == lane) {
+                    const double* l0 = LD + k * PLDL + b0;
+                    double s0 = row[k];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) s0 = fma(-v[i], l0[i], s0);
+                    row[k] = s0;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    // ---- L^-1: diagonal blocks, lane = (block bl, column c)
+    {
+        const int bl = lane >> 3, c = lane & 7, b0 = 8 * bl;
+        double x[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            double acc = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+            for (int k = 0; k < r; ++k) acc = fma(-LD[(b0 + r) * PLDL + b0 + k], x[k], acc);
+            x[r] = (r < c) ? 0.0 : acc * DINV[b0 + r];
+        }
+#pragma unroll 4
+        for (int r = 0; r < PNB; ++r) LI[r * PLD + lane] = 0.0;        // column `lane`
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 8; ++r) LI[(b0 + r) * PLD + b0 + c] = x[r];
+        __syncwarp();
+    }
+    // off-diagonal blocks by block diagonal d: (i, j) = (j + d, j)
+#pragma unroll 1
+    for (int d = 1; d < 4; ++d) {
+        const int nb = 4 - d;                       // blocks on this diagonal
+        if (lane < 8 * nb) {
+            const int jb = lane >> 3, c = lane & 7, ib = jb + d;
+            double t[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) t[r] = 0.0;
+            // t = sum_{k = jb .. ib-1} L_{ib,k} Linv_{k,jb}[:, c]
+            for (int kb = jb; kb < ib; ++kb) {
+                double y[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) y[q] = LI[(8 * kb + q) * PLD + 8 * jb + c];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const double* lr = LD + (8 * ib + r) * PLDL + 8 * kb;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) t[r] = fma(lr[q], y[q], t[r]);
+                }
+            }
+            // Linv_{ib,jb}[:, c] = -D^-1_ib t
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                double acc = 0.0;
+#pragma unroll
+                for (int q = 0; q <= r; ++q) acc = fma(LI[(8 * ib + r) * PLD + 8 * ib + q], t[q], acc);
+                LI[(8 * ib + r) * PLD + 8 * jb + c] = -acc;
+            }
+        }
+        __syncwarp();
+    }
+    return good;
 }
 
 template <bool VOXEL>
@@ -112,6 +273,7 @@ __global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, Pr
     int* QT = reinterpret_cast<int*>(smem + lay.QT);
     double* LD = smem + lay.LD;
     double* LI = smem + lay.LI;
+    double* BS = smem + lay.BS;
     double* Lw = pk.work + int64_t(team) * pk.per_team;
     double* part = pk.partial + int64_t(team) * pk.partial_per_team;
     const int num_items = VOXEL ? va.num_items : pa.num_items;
@@ -201,124 +363,164 @@ __global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, Pr
         };
 
         bool ok = false;
+        // ---- GEMM waves: P_pt (+)= M / - sum_{q in [q0, q1)} L[jt:, q-block] L[jt:jt+32, q-block]^T
+        // over 16x32 row tiles (two 8-row x four 8-column DMMA tiles per warp), in
+        // waves of one tile per participating warp of the team (warps w0..PW-1 of
+        // every CTA).  The B operand block L[jt:jt+32, 32q:32q+32] is staged once
+        // per CTA in shared memory by cp.async (double-buffered one block ahead);
+        // each warp's A fragments of block q+1 load into registers while block q's
+        // 64 DMMAs issue.  init: 0 -> M (generated), 1 -> P_pt from the workspace.
+        auto gemm_waves = [&](int pt, int q0, int q1, int init, int w0, double jit) {
+            const int jt = pt * PNB;
+            double* Pt = Lw + panel_base(R, pt);
+            const int ldt = R - jt;
+            const int T = (R - jt) / PRT;
+            const int wpc = PW - w0;                    // participating warps per CTA
+            const int nw = C * wpc;
+            const int gw = (crank * wpc + (warp - w0) + pt) % nw;
+            const int waves = (T + nw - 1) / nw;
+            const int nthr = wpc * 32, ltid = tid - w0 * 32;
+            auto bar = [&]() {
+                if (w0 == 0) __syncthreads();
+                else asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+            };
+            for (int w = 0; w < waves; ++w) {
+                const int t = w * nw + gw;
+                const bool act = t < T;
+                const int r0 = jt + (act ? t : 0) * PRT;
+                double acc[2][4][2];
+                double* dst = Pt + (r0 - jt) + g;
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            double v = 0.0;
+                            if (act)
+                                v = init ? __ldcg(dst + int64_t(8 * b + 2 * tig + e) * ldt + 8 * a)
+                                         : mval(r0 + 8 * a + g, jt + 8 * b + 2 * tig + e, jit);
+                            acc[a][b][e] = v;
+                        }
+                if (q1 > q0) {
+                    auto stage_b = [&](int q) {
+                        const int ldq = R - q * PNB;
+                        const double* src = Lw + panel_base(R, q) + (jt - q * PNB);
+                        double* bdst = BS + (q & 1) * (PNB * PLD);
+                        for (int e = ltid; e < PNB * 8; e += nthr) {
+                            const int k = e >> 3, r = (e & 7) * 4;
+                            cp_async16(bdst + k * PLD + r, src + int64_t(k) * ldq + r);
+                            cp_async16(bdst + k * PLD + r + 2, src + int64_t(k) * ldq + r + 2);
+                        }
+                        cp_async_commit();
+                    };
+                    auto load_a = [&](int q, double (&f)[2][8]) {
+                        const int ldq = R - q * PNB;
+                        const double* src = Lw + panel_base(R, q) + int64_t(tig) * ldq +
+                                            (r0 - q * PNB) + g;
+#pragma unroll
+                        for (int st = 0; st < 8; ++st)
+#pragma unroll
+                            for (int a = 0; a < 2; ++a)
+                                f[a][st] = act ? -__ldcg(src + int64_t(4 * st) * ldq + 8 * a) : 0.0;
+                    };
+                    double fa[2][8], na[2][8];
+                    stage_b(q0);
+                    load_a(q0, fa);
+                    for (int q = q0; q < q1; ++q) {
+                        cp_async_wait_all();
+                        bar();                        // BS[q & 1] complete; BS[(q+1) & 1] free
+                        if (q + 1 < q1) {
+                            stage_b(q + 1);
+                            load_a(q + 1, na);
+                        }
+                        const double* bs = BS + (q & 1) * (PNB * PLD) + tig * PLD + g;
+                        if (act)
+#pragma unroll
+                        for (int st = 0; st < 8; ++st) {
+                            double fb[4];
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) fb[b] = bs[4 * st * PLD + 8 * b];
+#pragma unroll
+                            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                                for (int b = 0; b < 4; ++b)
+                                    dmma_acc(acc[a][b][0], acc[a][b][1], fa[a][st], fb[b]);
+                        }
+                        if (q + 1 < q1) {
+#pragma unroll
+                            for (int st = 0; st < 8; ++st) {
+                                fa[0][st] = na[0][st];
+                                fa[1][st] = na[1][st];
+                            }
+                        }
+                    }
+                    bar();                            // BS reads done before the next wave
+                }
+                if (act) {
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e)
+                                __stcg(dst + int64_t(8 * b + 2 * tig + e) * ldt + 8 * a, acc[a][b][e]);
+                }
+            }
+        };
+
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? jitter : 0.0;
             ok = true;
+#ifdef VX_PHASE_TIMING
+            long long tph = clock64();
+#endif
+            // Look-ahead (teams of several CTAs, the latency regime): the bulk of
+            // panel p+1's update (A1, blocks < p) runs during panel p's diagonal
+            // chain and only the last block (A2) stays on the critical path.  One-CTA
+            // teams (the throughput regime, two CTAs per SM) update each panel in
+            // one pass with all warps: the other CTA of the SM covers the chain, and
+            // the look-ahead's extra pass over P and its 7-warp waves cost more.
+            const bool ahead = C > 1;
+            if (ahead) {                              // P_0 = M[:, 0:32]
+                gemm_waves(0, 0, 0, 0, 0, jit);
+                team_sync(C);
+            }
             for (int p = 0; p < np; ++p) {
                 const int j = p * PNB;
                 double* Pp = Lw + panel_base(R, p);
                 const int ldp = R - j;
-                // ---- phase A: P = M[j:, j:j+32] - L[j:, :j] L[j:j+32, :j]^T in 16x32
-                // row tiles (two 8-row DMMA tiles x four 8-column tiles per warp)
-                const int T = (R - j) / PRT;
-                const int nw = C * PW;
-                const int gw = (crank * PW + warp + p) % nw;
-                for (int t = gw; t < T; t += nw) {
-                    const int r0 = j + t * PRT;
-                    double acc[2][4][2];
-#pragma unroll
-                    for (int a = 0; a < 2; ++a)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e)
-                                acc[a][b][e] = mval(r0 + 8 * a + g, j + 8 * b + 2 * tig + e, jit);
-                    // k runs over the finished panels q < p (columns 32q .. 32q+31);
-                    // software-pipelined: the fragments of step s+1 load while the
-                    // DMMAs of step s issue
-                    const int steps = p * (PNB / 4);
-                    auto frag_ptr = [&](int st, int row0) {
-                        const int q = st >> 3, kk = (st & 7) * 4;
-                        const int ldq = R - q * PNB;
-                        return Lw + panel_base(R, q) + int64_t(kk + tig) * ldq + (row0 - q * PNB) + g;
-                    };
-                    double fa[2], fb[4];
-                    if (steps > 0) {
-                        const double* pa_ = frag_ptr(0, r0);
-                        const double* pb_ = frag_ptr(0, j);
-                        fa[0] = __ldcg(pa_);
-                        fa[1] = __ldcg(pa_ + 8);
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) fb[b] = __ldcg(pb_ + 8 * b);
-                    }
-                    for (int st = 0; st < steps; ++st) {
-                        double na[2] = {0.0, 0.0}, nb[4] = {0.0, 0.0, 0.0, 0.0};
-                        if (st + 1 < steps) {
-                            const double* pa_ = frag_ptr(st + 1, r0);
-                            const double* pb_ = frag_ptr(st + 1, j);
-                            na[0] = __ldcg(pa_);
-                            na[1] = __ldcg(pa_ + 8);
-#pragma unroll
-                            for (int b = 0; b < 4; ++b) nb[b] = __ldcg(pb_ + 8 * b);
-                        }
-#pragma unroll
-                        for (int a = 0; a < 2; ++a)
-#pragma unroll
-                            for (int b = 0; b < 4; ++b) dmma_acc(acc[a][b][0], acc[a][b][1], -fa[a], fb[b]);
-                        fa[0] = na[0];
-                        fa[1] = na[1];
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) fb[b] = nb[b];
-                    }
-                    double* dst = Pp + (r0 - j) + g;
-#pragma unroll
-                    for (int a = 0; a < 2; ++a)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e)
-                                __stcg(dst + int64_t(8 * b + 2 * tig + e) * ldp + 8 * a, acc[a][b][e]);
+                // ---- (A) P_p = M - L[j:, :j] L[j:j+32, :j]^T; with look-ahead only the
+                // last finished panel p-1 remains (A2), the earlier blocks were applied
+                // by (A1) during panel p-1's diagonal chain
+                if (!ahead || p > 0) {
+                    if (ahead) gemm_waves(p, p - 1, p, 1, 0, jit);
+                    else gemm_waves(p, 0, p, 0, 0, jit);
+                    VX_PHASE(12, tph);                // phase A / A2
+                    team_sync(C);
+                    VX_PHASE(13, tph);                // team barrier after A
                 }
-                team_sync(C);
-                // ---- phase B (1): every CTA factors the diagonal block (warp 0).
-                // Left-looking, row r by lane r, rows in shared memory (LD, stride
-                // PLDL: conflict-free row reads); then column c of L_dd^-1 by lane c
-                // into LI (row-major).  A pivot that is not > 0 fails (dpotrf).
+                // ---- (D) warp 0 of every CTA factors the diagonal block (redundantly:
+                // every CTA takes the same pivot decision) while warps 1..7 run (A1),
+                // the look-ahead: P_{p+1} = M - (blocks 0 .. p-1), which do not depend
+                // on panel p
                 if (warp == 0) {
-                    double* myrow = LD + lane * PLDL;
-#pragma unroll 4
-                    for (int c = 0; c < PNB; ++c) myrow[c] = __ldcg(Pp + int64_t(c) * ldp + lane);
-                    __syncwarp();
-                    bool good = true;
-                    for (int c = 0; c < PNB; ++c) {
-                        const double* rowc = LD + c * PLDL;
-                        double s0 = myrow[c], s1 = 0.0;
-                        int k = 0;
-                        for (; k + 1 < c; k += 2) {
-                            s0 = fma(-myrow[k], rowc[k], s0);
-                            s1 = fma(-myrow[k + 1], rowc[k + 1], s1);
-                        }
-                        if (k < c) s0 = fma(-myrow[k], rowc[k], s0);
-                        const double sc = s0 + s1;
-                        const double piv = __shfl_sync(FULL, sc, c);
-                        if (!(piv > 0.0)) good = false;
-                        const double d = sqrt(piv);
-                        __syncwarp();
-                        myrow[c] = lane == c ? d : (lane > c ? sc / d : 0.0);
-                        __syncwarp();
-                    }
-                    // x = column `lane` of L_dd^-1: x_r = (e_r - sum_{k<r} L(r,k) x_k) / L(r,r)
-                    for (int r = 0; r < PNB; ++r) {
-                        const double* rowr = LD + r * PLDL;
-                        double s0 = (r == lane) ? 1.0 : 0.0, s1 = 0.0;
-                        int k = lane;                      // x_k = 0 for k < lane
-                        for (; k + 1 < r; k += 2) {
-                            s0 = fma(-rowr[k], LI[k * PLD + lane], s0);
-                            s1 = fma(-rowr[k + 1], LI[(k + 1) * PLD + lane], s1);
-                        }
-                        if (k < r) s0 = fma(-rowr[k], LI[k * PLD + lane], s0);
-                        LI[r * PLD + lane] = r < lane ? 0.0 : (s0 + s1) / rowr[r];
-                    }
+                    const bool good = diag_block_factor(Pp, ldp, LD, LI, smem + lay.DINV, lane);
                     if (lane == 0) smem[lay.FLAG] = good ? 1.0 : 0.0;
+                } else if (ahead && p + 1 < np) {
+                    gemm_waves(p + 1, 0, p, 0, 1, jit);
                 }
                 __syncthreads();
-                if (smem[lay.FLAG] == 0.0) {      // the same decision in every CTA
+                VX_PHASE(14, tph);                    // diagonal || look-ahead
+                if (smem[lay.FLAG] == 0.0) {          // the same decision in every CTA
                     ok = false;
                     team_sync(C);
                     break;
                 }
-                // ---- phase B (2): L[j+32:, j:j+32] = P[32:] L_dd^-T (DMMA with L_dd^-1)
-                const int T2 = T - PNB / PRT;
+                // ---- (B) L[j+32:, j:j+32] = P[32:] L_dd^-T (DMMA with L_dd^-1)
+                const int T2 = (R - j) / PRT - PNB / PRT;
+                const int nw = C * PW;
+                const int gw = (crank * PW + warp + p) % nw;
                 for (int t = gw; t < T2; t += nw) {
                     double* src = Pp + PNB + t * PRT + g;
                     double fa2[2][8];
@@ -350,7 +552,9 @@ __global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, Pr
                             for (int e = 0; e < 2; ++e)
                                 __stcg(src + int64_t(8 * b + 2 * tig + e) * ldp + 8 * a, acc[a][b][e]);
                 }
+                VX_PHASE(15, tph);                    // phase B triangular update
                 team_sync(C);
+                VX_PHASE(16, tph);                    // team barrier after B
             }
         }
         if (!ok) {
