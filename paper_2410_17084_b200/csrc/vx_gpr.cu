@@ -2955,6 +2955,13 @@ int launch_voxel_solve(const VoxelSolveArgs& a, int max_n, DevBuf& work, cudaStr
         set_error("n_s * n_r = %d exceeds %d", mm, MAX_MM);
         return VX_E_INPUT;
     }
+    // A/B hook: VX_PANEL_FROM=k routes the tile buckets whose lower bound is >= k
+    // (64, 96, 128) to the panel kernel
+    if (const char* e = getenv("VX_PANEL_FROM")) {
+        const int from = atoi(e);
+        const int lo = bucket == 6 ? 64 : bucket == 3 ? 96 : bucket == 7 ? 128 : -1;
+        if (lo >= 0 && lo >= from) return launch_panel<true>(a, none, a.num_items, max_n, a.M, mm, work, s);
+    }
     switch (bucket) {
         case 0: return launch_wdmma<16>(a, mm, s);
         case 1: return launch_wdmma<24>(a, mm, s);

@@ -59,7 +59,8 @@ struct VxMap {
     int64_t first_count = 0;   // first solves of the last ingest, listed in `items`
     // counters (device) + pinned mirror
     vx::DevBuf counters;
-    int64_t* host_counters = nullptr;
+    int64_t* host_counters = nullptr;      // mapped pinned memory (see read_counters)
+    int64_t* host_counters_dev = nullptr;  // its device alias
     // temporaries
     vx::DevBuf scan_tmp, sort_tmp, gpr_work, stage;
 };
@@ -395,9 +396,19 @@ static int grow_array(DevBuf& b, int64_t old_n, int64_t new_n, cudaStream_t s) {
     return VX_OK;
 }
 
+// The counters cross to the host through MAPPED pinned memory, written by a
+// one-warp kernel, not by cudaMemcpyAsync: a copy would queue on the copy
+// engine behind whatever bulk transfer is in flight (the next frame's H2D, the
+// previous frame's record D2H in MappingEngine.ingest_stream), and each of the
+// ingest's counter reads would wait for it.
+__global__ void k_copy_i64(int64_t* __restrict__ dst, const int64_t* __restrict__ src, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
 static int read_counters(VxMap* m, cudaStream_t s) {
-    VX_CUDA(cudaMemcpyAsync(m->host_counters, m->counters.ptr, C_COUNT * sizeof(int64_t),
-                            cudaMemcpyDeviceToHost, s));
+    k_copy_i64<<<1, 64, 0, s>>>(m->host_counters_dev, m->counters.as<int64_t>(), C_COUNT);
+    count_launch();
+    VX_CHECK_LAUNCH();
     VX_CUDA(cudaStreamSynchronize(s));
     return VX_OK;
 }
@@ -750,8 +761,10 @@ static int map_densify_impl(VxMap* m, VxDensifyInfo* info, cudaStream_t s) {
         acc += counts[b];
         m->host_counters[C_O0 + b] = offs[b];
     }
-    VX_CUDA(cudaMemcpyAsync(ctr(m) + C_O0, m->host_counters + C_O0, NUM_BUCKETS * sizeof(int64_t),
-                            cudaMemcpyHostToDevice, s));
+    // (host -> device through the mapped counters, off the copy engines)
+    k_copy_i64<<<1, 32, 0, s>>>(reinterpret_cast<int64_t*>(ctr(m)) + C_O0, m->host_counters_dev + C_O0,
+                                NUM_BUCKETS);
+    count_launch();
     VX_TRY(launch_bucket_items(a, int(S), m->items.as<int32_t>(), ctr(m) + C_O0, ctr(m) + C_F0, s));
     // largest buckets first so their tails overlap the small ones
     for (int b = NUM_BUCKETS - 1; b >= 0; --b) {
@@ -855,7 +868,9 @@ VxMap* map_new(const VxMapConfig& cfg, int* rc) {
     cudaStream_t s = 0;
     int r = VX_OK;
     if ((r = m->counters.reserve(C_COUNT * sizeof(int64_t), s)) != VX_OK ||
-        cudaMallocHost(&m->host_counters, C_COUNT * sizeof(int64_t)) != cudaSuccess ||
+        cudaHostAlloc(&m->host_counters, C_COUNT * sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&m->host_counters_dev), m->host_counters, 0) !=
+            cudaSuccess ||
         (r = ensure_voxels(m, std::max<int64_t>(cfg.voxel_capacity, 1024), s)) != VX_OK ||
         (r = ensure_arena(m, std::max<int64_t>(cfg.point_capacity, 1 << 16), s)) != VX_OK ||
         (r = rebuild_table(m, 2 * std::max<int64_t>(cfg.voxel_capacity, 1024), s)) != VX_OK) {
