@@ -3020,3 +3020,37 @@ extern "C" int vx_phase_cycles(unsigned long long* out, int max_phases) {
     return k;
 }
 #endif
+
+#ifdef VX_PHASE_TIMING
+// diagnostics-build microbenchmark: cycles of one diag_block_factor call (one
+// warp, 32x32 SPD block in global memory, repeated `iters` times)
+namespace vx {
+__global__ void k_diag_bench(const double* P, int iters, unsigned long long* out) {
+    extern __shared__ __align__(16) double sm[];
+    double* LD = sm;
+    double* LI = sm + PNB * PLD;
+    double* DINV = LI + PNB * PLD;
+    const int lane = threadIdx.x & 31;
+    bool ok = true;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) ok &= diag_block_factor(P, PNB, LD, LI, DINV, lane);
+    const long long t1 = clock64();
+    if (lane == 0) out[0] = (unsigned long long)(t1 - t0) / iters + (ok ? 0 : 1ull << 62);
+}
+}  // namespace vx
+extern "C" int vx_diag_bench(int iters, unsigned long long* cycles) {
+    double h[32 * 32];
+    for (int c = 0; c < 32; ++c)
+        for (int r = 0; r < 32; ++r) h[c * 32 + r] = (r == c ? 40.0 : 1.0 / (1.0 + r + c));
+    double* d = nullptr;
+    unsigned long long* o = nullptr;
+    cudaMalloc(&d, sizeof(h));
+    cudaMalloc(&o, 8);
+    cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
+    vx::k_diag_bench<<<1, 32, (2 * 32 * vx::PLD + 32) * 8>>>(d, iters, o);
+    cudaMemcpy(cycles, o, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    cudaFree(o);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -24,11 +24,10 @@ hdr = rows[0]
 col = {h: i for i, h in enumerate(hdr)}
 _, _, counts, *_ = bench.make_workload(V, 0)
 sol = counts[counts >= bench.TAU]
-# launch order within one densify is bucket id 7, 6, 5, 4, 3, 2, 1, 0 (largest first)
-buckets = [("gpr_big_kernel<12", (128, 160), "gpr_n160"),
+buckets = [("gpr_tile_kernel<20,", (128, 160), "gpr_n160"),
            ("gpr_tile_kernel<12,", (64, 96), "gpr_n96"),
            ("gpr_wdmma_kernel<32", (24, 32), "gpr_n32"),
-           ("gpr_big_kernel<12", (160, 10 ** 9), "gpr_n_large"),
+           ("gpr_panel_kernel", (160, 10 ** 9), "gpr_n_large"),
            ("gpr_tile_kernel<16, 1, 6", (96, 128), "gpr_n128"),
            ("gpr_tile_kernel<8,", (32, 64), "gpr_n64"),
            ("gpr_wdmma_kernel<24", (16, 24), "gpr_n24"),
