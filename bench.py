@@ -107,7 +107,7 @@ class Clocks:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -566,10 +566,11 @@ def run_gpu(args, rank, world, local_rank):
                 pass
         return float(t.item()), reps, launches, prof
 
+    # clocks sampled over both timed regions (device steps and the e2e stream)
     clocks = Clocks(local_rank)
     clocks.start()
+    time.sleep(0.3)                 # nvidia-smi up before the timed region
     ms, reps, launches, prof = timed(step_device, args.steps, profile=True)
-    clk = clocks.stop()
     solved = sum(r.voxels_solved for r in reps) / args.steps
     tot_solved = torch.tensor([solved], dtype=torch.float64, device=dev)
     if world > 1:
@@ -581,6 +582,7 @@ def run_gpu(args, rank, world, local_rank):
     e2e_ms, e2e_reps, _, _ = timed(lambda: run_e2e(args.steps), 1)
     e2e_wall_ms = (time.perf_counter() - t_wall) * 1e3
     e2e_value = float(tot_solved.item()) / (e2e_ms / args.steps / 1e3)
+    clk = clocks.stop()
     res_ms, _, _, _ = timed(lambda: run_e2e_resident(args.steps), 1)
     h2d = h_xyz.numel() * 8 + h_rgb.numel() * 8 + h_img.numel() * 8
     # Gaussian records of the frame (136 B each) + frame/densify info structs
