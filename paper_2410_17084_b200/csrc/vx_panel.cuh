@@ -110,22 +110,65 @@ __device__ __forceinline__ unsigned cluster_rank() {
 // diagonal), DINV[r] = 1 / L_dd(r, r); returns false when a pivot is not > 0
 // (dpotrf's failure rule, gpr.py:187-192).
 //
-// Blocked right-looking by 8 columns: every lane factors the 8x8 diagonal
-// block in its own registers (dpotf2 order: pivot p, l = 1/sqrt(p) scaling,
-// rank-1 update; the reciprocal square root is the only transcendental and
-// there is no division), the lanes of the rows below solve their row against
-// it and apply the block's rank-8 update to the rest of their row.  L_dd^-1:
-// lane (block, column) forms column `column` of the 8x8 block inverse, then the
+// Left-looking by 8-column blocks, lane = row: the block loads with one
+// asynchronous copy wave; per block column the rows at or below it apply the
+// finished columns (8 independent FMA chains per lane, the finished rows read
+// as shared-memory broadcasts), every lane factors the 8x8 diagonal block in
+// its own registers (dpotf2 order: pivot p, scale by 1/sqrt(p), rank-1 update;
+// the reciprocal square root is the only transcendental, there is no
+// division) and the rows below solve against it in registers.  L_dd^-1: lane
+// (block, column) forms column `column` of the 8x8 block inverse, then the
 // off-diagonal blocks by block diagonal, L^-1_ij = -D^-1_i sum_k L_ik L^-1_kj.
+#ifdef VX_PHASE_TIMING
+__device__ unsigned long long g_diag_t[8];
+#define DIAG_T(i) do { if (lane == 0) { g_diag_t[i] += clock64() - t_; t_ = clock64(); } } while (0)
+#else
+#define DIAG_T(i) do { } while (0)
+#endif
 __device__ __noinline__ bool diag_block_factor(const double* __restrict__ P, int ldp, double* LD,
                                                double* LI, double* DINV, int lane) {
-#pragma unroll 4
-    for (int c = 0; c < PNB; ++c) LD[lane * PLDL + c] = __ldcg(P + int64_t(c) * ldp + lane);
-    __syncwarp();
+#ifdef VX_PHASE_TIMING
+    long long t_ = clock64();
+#endif
+    // P -> LD (row-major, stride PLDL): 32 asynchronous 8-byte copies per lane,
+    // one wait (one L2 round trip instead of one per load batch)
+    {
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(LD + lane * PLDL));
+#pragma unroll
+        for (int c = 0; c < PNB; ++c)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 8u * c),
+                         "l"(P + int64_t(c) * ldp + lane) : "memory");
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+    }
+    DIAG_T(0);
     bool good = true;
+    // Left-looking by 8-column blocks: lane = row.  (1) rows >= b0 apply every
+    // finished block column to their block-column-kb entries (8 independent
+    // accumulators per lane, the finished rows read as broadcasts); (2) every
+    // lane factors the 8x8 diagonal block in registers; (3) the rows below
+    // solve against it in registers.
 #pragma unroll 1
     for (int kb = 0; kb < 4; ++kb) {
         const int b0 = 8 * kb;
+        double v[8];
+        const bool mine = lane >= b0;
+        double* row = LD + lane * PLDL;
+        if (mine) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = row[b0 + c];
+#pragma unroll 4
+            for (int i = 0; i < b0; ++i) {
+                const double li = row[i];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) v[c] = fma(-li, LD[(b0 + c) * PLDL + i], v[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) row[b0 + c] = v[c];
+        }
+        __syncwarp();
+        DIAG_T(1);
         double a[36];
 #pragma unroll
         for (int r = 0; r < 8; ++r)
@@ -148,57 +191,27 @@ __device__ __noinline__ bool diag_block_factor(const double* __restrict__ P, int
                                                  a[r * (r + 1) / 2 + k]);
         }
         __syncwarp();
-        // the block's own rows (lane in [b0, b0 + 8)) and 1/L_rr
+        DIAG_T(2);
+        // every row at or below the block solves its 8 entries against the factor:
+        // for the block's own rows this reproduces the factorisation operation for
+        // operation (the same FMAs in the same order; the diagonal comes out as
+        // piv * 1/sqrt(piv)), so no lane has to publish from the replicated a[]
+        if (mine) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
-            if (lane == b0 + r) {
+            for (int c = 0; c < 8; ++c) {
+                v[c] *= inv[c];
 #pragma unroll
-                for (int c = 0; c <= r; ++c) LD[lane * PLDL + b0 + c] = a[r * (r + 1) / 2 + c];
-                DINV[lane] = inv[r];
+                for (int k = c + 1; k < 8; ++k) v[k] = fma(-v[c], a[k * (k + 1) / 2 + c], v[k]);
             }
-        if (kb < 3) {
-            const bool below = lane >= b0 + 8;
-            double v[8];
-            if (below) {
-                double* row = LD + lane * PLDL + b0;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) v[c] = row[c];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    v[c] *= inv[c];
-#pragma unroll
-                    for (int k = c + 1; k < 8; ++k) v[k] = fma(-v[c], a[k * (k + 1) / 2 + c], v[k]);
-                }
-#pragma unroll
-                for (int c = 0; c < 8; ++c) row[c] = v[c];
-            }
-            __syncwarp();
-            // rank-8 update of the rest of the row: LD[r][k] -= sum_i L[r][b0+i] L[k][b0+i]
-            if (below) {
-                double* row = LD + lane * PLDL;
-                int k = b0 + 8;
-                for (; k + 1 <= lane; k += 2) {
-                    const double* l0 = LD + k * PLDL + b0;
-                    const double* l1 = l0 + PLDL;
-                    double s0 = row[k], s1 = row[k + 1];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        s0 = fma(-v[i], l0[i], s0);
-                        s1 = fma(-v[i], l1[i], s1);
-                    }
-                    row[k] = s0;
-                    row[k + 1] = s1;
-                }
-                if (k == lane) {
-                    const double* l0 = LD + k * PLDL + b0;
-                    double s0 = row[k];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) s0 = fma(-v[i], l0[i], s0);
-                    row[k] = s0;
-                }
-            }
-            __syncwarp();
+            for (int c = 0; c < 8; ++c) row[b0 + c] = v[c];
         }
+        double di = 0.0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) di = lane == b0 + r ? inv[r] : di;
+        if (lane >= b0 && lane < b0 + 8) DINV[lane] = di;
+        __syncwarp();
+        DIAG_T(3);
     }
     // ---- L^-1: diagonal blocks, lane = (block bl, column c)
     {
@@ -218,6 +231,7 @@ __device__ __noinline__ bool diag_block_factor(const double* __restrict__ P, int
         for (int r = 0; r < 8; ++r) LI[(b0 + r) * PLD + b0 + c] = x[r];
         __syncwarp();
     }
+    DIAG_T(4);
     // off-diagonal blocks by block diagonal d: (i, j) = (j + d, j)
 #pragma unroll 1
     for (int d = 1; d < 4; ++d) {
@@ -250,6 +264,7 @@ __device__ __noinline__ bool diag_block_factor(const double* __restrict__ P, int
         }
         __syncwarp();
     }
+    DIAG_T(5);
     return good;
 }
 

@@ -12,3 +12,10 @@ out = ctypes.c_ulonglong(0)
 for iters in (1, 10, 100):
     lib.vx_diag_bench(iters, ctypes.byref(out))
     print(f"iters {iters}: {out.value & ((1 << 62) - 1)} cycles per call, ok={not (out.value >> 62)}")
+
+parts = (ctypes.c_ulonglong * 8)()
+lib.vx_diag_parts(parts)
+lib.vx_diag_bench(100, ctypes.byref(out))
+lib.vx_diag_parts(parts)
+names = ("load", "update", "factor8", "solve+publish", "inv_diag", "inv_offdiag")
+print("per call:", {n: parts[i] // 100 for i, n in enumerate(names)})
