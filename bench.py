@@ -470,7 +470,7 @@ def run_gpu(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     N.lib()
 
-    pos, col, counts, keys, owner, cam_d, img = make_workload(args.voxels, rank)
+    pos, col, counts, keys, owner, cam_d, img = make_workload(args.voxels, 0)      # ONE map, sharded over the ranks
     npts = len(pos)
     cam = vx.Camera(cam_d["fx"], cam_d["fy"], cam_d["cx"], cam_d["cy"], cam_d["width"],
                     cam_d["height"], cam_d["R"], cam_d["t"])
@@ -592,7 +592,13 @@ def run_gpu(args, rank, world, local_rank):
     stages = {k: v for k, v in prof.items() if k != "densify" and v[1] > 0}
     top = max(stages, key=lambda k: stages[k][0])
     top_ms, top_n = stages[top]
-    sol = counts[counts >= TAU]
+    # this rank's share of the work (a hash-sharded map: the voxels it owns)
+    counts_r, npts_r = counts, npts
+    if world > 1:
+        from paper_2410_17084_b200 import sharding as _sh
+        counts_r = counts[_sh.owner_of(keys, world) == rank]
+        npts_r = int(counts_r.sum())
+    sol = counts_r[counts_r >= TAU]
     bucket = buckets_of(sol)
     if top in bucket:
         flops = float(gpr_flops(bucket[top]).sum()) * args.steps
@@ -617,14 +623,14 @@ def run_gpu(args, rank, world, local_rank):
                 "share_of_step": top_ms / ms}
     else:
         # hashing / splat are HBM-bound: algorithmic bytes per point = 104
-        bts = (104.0 * npts if top == "hash" else 1224.0 * solved_expected) * args.steps
+        bts = (104.0 * npts_r if top == "hash" else 1224.0 * len(sol)) * args.steps
         achieved = bts / (top_ms / 1e3) / 1e9
         pk = float(peaks.get("hbm_gbs", 6548.8))
         roof = {"kernel": top, "bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s",
                 "frac": achieved / pk, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "traffic": None, "launch_ms": top_ms / top_n, "share_of_step": top_ms / ms}
     hbm = float(peaks.get("hbm_gbs", 6548.8))
-    stage_ms, stage_roofline = stage_report(prof, counts, npts, args.steps, peak64, hbm)
+    stage_ms, stage_roofline = stage_report(prof, counts_r, npts_r, args.steps, peak64, hbm)
 
     # N > 1: the one collective of the path, the hand-off of the
     # frame's predictions and Gaussian records from every shard to rank 0
@@ -681,7 +687,8 @@ def run_gpu(args, rank, world, local_rank):
                                    f"Gaussian init for all first solves)",
                        "voxels": args.voxels, "points": npts,
                        "solved_per_step": float(tot_solved.item()),
-                       "l2": "inputs 1.2 GB > 126 MB L2, no flush",
+                       "l2": (f"inputs {48 * npts / 1e9:.2f} GB > 126 MB L2, no flush"
+                              if 48 * npts > 126e6 else "inputs fit in L2"),
                        "parallelism": (f"hash-shard x{world}: one map, voxels owned by "
                                        f"mix64(key) % {world}, whole scan on every rank"
                                        if world > 1 else "single GPU")},
