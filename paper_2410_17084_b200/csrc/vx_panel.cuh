@@ -107,7 +107,8 @@ __device__ __forceinline__ unsigned cluster_rank() {
 // all take the same pivot decision).  In: the block P at panel storage `P`
 // (column-major, ld `ldp`, lower part used).  Out: LD = L_dd (row-major,
 // stride PLDL, lower), LI = L_dd^-1 (row-major, stride PLD, zeros above the
-// diagonal), DINV[r] = 1 / L_dd(r, r); returns false when a pivot is not > 0
+// diagonal; only its four 8x8 diagonal blocks are formed), DINV[r] =
+// 1 / L_dd(r, r); returns false when a pivot is not > 0
 // (dpotrf's failure rule, gpr.py:187-192).
 //
 // Left-looking by 8-column blocks, lane = row: the block loads with one
@@ -116,9 +117,9 @@ __device__ __forceinline__ unsigned cluster_rank() {
 // as shared-memory broadcasts), every lane factors the 8x8 diagonal block in
 // its own registers (dpotf2 order: pivot p, scale by 1/sqrt(p), rank-1 update;
 // the reciprocal square root is the only transcendental, there is no
-// division) and the rows below solve against it in registers.  L_dd^-1: lane
-// (block, column) forms column `column` of the 8x8 block inverse, then the
-// off-diagonal blocks by block diagonal, L^-1_ij = -D^-1_i sum_k L_ik L^-1_kj.
+// division) and the rows below solve against it in registers.  Then the
+// inverses of the four 8x8 diagonal blocks (lane = (block, column)), which
+// phase B applies blockwise.
 #ifdef VX_PHASE_TIMING
 __device__ unsigned long long g_diag_t[8];
 #define DIAG_T(i) do { if (lane == 0) { g_diag_t[i] += clock64() - t_; t_ = clock64(); } } while (0)
@@ -232,38 +233,7 @@ __device__ __noinline__ bool diag_block_factor(const double* __restrict__ P, int
         __syncwarp();
     }
     DIAG_T(4);
-    // off-diagonal blocks by block diagonal d: (i, j) = (j + d, j)
-#pragma unroll 1
-    for (int d = 1; d < 4; ++d) {
-        const int nb = 4 - d;                       // blocks on this diagonal
-        if (lane < 8 * nb) {
-            const int jb = lane >> 3, c = lane & 7, ib = jb + d;
-            double t[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) t[r] = 0.0;
-            // t = sum_{k = jb .. ib-1} L_{ib,k} Linv_{k,jb}[:, c]
-            for (int kb = jb; kb < ib; ++kb) {
-                double y[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) y[q] = LI[(8 * kb + q) * PLD + 8 * jb + c];
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const double* lr = LD + (8 * ib + r) * PLDL + 8 * kb;
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) t[r] = fma(lr[q], y[q], t[r]);
-                }
-            }
-            // Linv_{ib,jb}[:, c] = -D^-1_ib t
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                double acc = 0.0;
-#pragma unroll
-                for (int q = 0; q <= r; ++q) acc = fma(LI[(8 * ib + r) * PLD + 8 * ib + q], t[q], acc);
-                LI[(8 * ib + r) * PLD + 8 * jb + c] = -acc;
-            }
-        }
-        __syncwarp();
-    }
+    // (the off-diagonal blocks of L_dd^-1 are not needed: phase B solves blockwise)
     DIAG_T(5);
     return good;
 }
@@ -532,32 +502,55 @@ __global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, Pr
                     team_sync(C);
                     break;
                 }
-                // ---- (B) L[j+32:, j:j+32] = P[32:] L_dd^-T (DMMA with L_dd^-1)
+                // ---- (B) L[j+32:, j:j+32] = P[32:] L_dd^-T, blockwise by 8 columns with
+                // DMMA: X_kb = (P_kb - sum_{i<kb} X_i L_{kb,i}^T) D_kb^-T, D_kb^-1 the
+                // 8x8 diagonal-block inverses (no off-diagonal inverse on the chain).
+                // Accumulators (C layout) become A operands by two shuffles per value.
                 const int T2 = (R - j) / PRT - PNB / PRT;
                 const int nw = C * PW;
                 const int gw = (crank * PW + warp + p) % nw;
+                // A fragment (k-chunk sl) of an 8x8 C-layout block held as (c0, c1)
+                auto c_to_a = [&](double c0, double c1, int sl) {
+                    const int srcl = g * 4 + 2 * sl + (tig >> 1);
+                    const double v0 = __shfl_sync(FULL, c0, srcl);
+                    const double v1 = __shfl_sync(FULL, c1, srcl);
+                    return (tig & 1) ? v1 : v0;
+                };
                 for (int t = gw; t < T2; t += nw) {
                     double* src = Pp + PNB + t * PRT + g;
-                    double fa2[2][8];
+                    double pc[2][4][2];
 #pragma unroll
                     for (int a = 0; a < 2; ++a)
 #pragma unroll
-                        for (int kc = 0; kc < 8; ++kc)
-                            fa2[a][kc] = __ldcg(src + int64_t(4 * kc + tig) * ldp + 8 * a);
-                    double acc[2][4][2];
+                        for (int b = 0; b < 4; ++b)
 #pragma unroll
-                    for (int a = 0; a < 2; ++a)
+                            for (int e = 0; e < 2; ++e)
+                                pc[a][b][e] = __ldcg(src + int64_t(8 * b + 2 * tig + e) * ldp + 8 * a);
+                    double xa[2][4][2];       // X_i as A fragments (k-chunks 0, 1)
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+                    for (int kb = 0; kb < 4; ++kb) {
 #pragma unroll
-                    for (int kc = 0; kc < 8; ++kc) {
-                        double fb[4];
+                        for (int a = 0; a < 2; ++a) {
+                            double c0 = pc[a][kb][0], c1 = pc[a][kb][1];
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) fb[b] = LI[(8 * b + g) * PLD + 4 * kc + tig];
+                            for (int i = 0; i < kb; ++i)
 #pragma unroll
-                        for (int a = 0; a < 2; ++a)
+                                for (int sl = 0; sl < 2; ++sl)
+                                    dmma_acc(c0, c1, -xa[a][i][sl],
+                                             LD[(8 * kb + g) * PLDL + 8 * i + 4 * sl + tig]);
+                            // X = C D^-T: B[q][c] = D^-1[c][q]
+                            double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-                            for (int b = 0; b < 4; ++b) dmma_acc(acc[a][b][0], acc[a][b][1], fa2[a][kc], fb[b]);
+                            for (int sl = 0; sl < 2; ++sl)
+                                dmma_acc(d0, d1, c_to_a(c0, c1, sl),
+                                         LI[(8 * kb + g) * PLD + 8 * kb + 4 * sl + tig]);
+                            pc[a][kb][0] = d0;
+                            pc[a][kb][1] = d1;
+                            if (kb < 3) {
+#pragma unroll
+                                for (int sl = 0; sl < 2; ++sl) xa[a][kb][sl] = c_to_a(d0, d1, sl);
+                            }
+                        }
                     }
 #pragma unroll
                     for (int a = 0; a < 2; ++a)
@@ -565,7 +558,7 @@ __global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, Pr
                         for (int b = 0; b < 4; ++b)
 #pragma unroll
                             for (int e = 0; e < 2; ++e)
-                                __stcg(src + int64_t(8 * b + 2 * tig + e) * ldp + 8 * a, acc[a][b][e]);
+                                __stcg(src + int64_t(8 * b + 2 * tig + e) * ldp + 8 * a, pc[a][b][e]);
                 }
                 VX_PHASE(15, tph);                    // phase B triangular update
                 team_sync(C);
