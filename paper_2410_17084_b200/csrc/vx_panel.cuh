@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, Pr
                             if (act)
                                 v = init ? __ldcg(dst + int64_t(8 * b + 2 * tig + e) * ldt + 8 * a)
                                          : mval(r0 + 8 * a + g, jt + 8 * b + 2 * tig + e, jit);
-                            acc[a][b][e] = v;
+                            acc[a][b][e] = -v;        // accumulate -P: the fragments stay un-negated
+
                         }
                 if (q1 > q0) {
                     auto stage_b = [&](int q) {
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, Pr
                         for (int st = 0; st < 8; ++st)
 #pragma unroll
                             for (int a = 0; a < 2; ++a)
-                                f[a][st] = act ? -__ldcg(src + int64_t(4 * st) * ldq + 8 * a) : 0.0;
+                                f[a][st] = act ? __ldcg(src + int64_t(4 * st) * ldq + 8 * a) : 0.0;
                     };
                     double fa[2][8], na[2][8];
                     stage_b(q0);
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(PNT, 2) gpr_panel_kernel(VoxelSolveArgs va, Pr
                         for (int b = 0; b < 4; ++b)
 #pragma unroll
                             for (int e = 0; e < 2; ++e)
-                                __stcg(dst + int64_t(8 * b + 2 * tig + e) * ldt + 8 * a, acc[a][b][e]);
+                                __stcg(dst + int64_t(8 * b + 2 * tig + e) * ldt + 8 * a, -acc[a][b][e]);
                 }
             }
         };
