@@ -1370,6 +1370,7 @@ gpr_wdmma_kernel(VoxelSolveArgs va, int mmax, int mm) {
         // ---- A = K + diag(noise), right-looking Cholesky in registers, one
         //      jitter retry (gpr.py:184-194)
         bool ok = false;
+        double a[NMAX];
         for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
             const double jit = attempt ? va.jitter : 0.0;
             const int ntri = n * (n - 1) / 2;
@@ -1384,11 +1385,15 @@ gpr_wdmma_kernel(VoxelSolveArgs va, int mmax, int mm) {
                 if (jit != 0.0) dg = xadd(dg, jit);
             }
             __syncwarp();
-            double a[NMAX];
+            // NMAX == 16: lanes 16 + c carry the augmented row e_c^T through the
+            // same right-looking sweep, which leaves column c of L^-1 in their
+            // registers (the forward substitution L x = e_c in the order and
+            // roundings of the separate lane-per-column pass it replaces)
 #pragma unroll
             for (int k = 0; k < NMAX; ++k) {
                 double v = 0.0;
-                if (k == lane) v = dg;
+                if (NMAX == 16 && lane >= 16) v = (k == lane - 16) ? 1.0 : 0.0;
+                else if (k == lane) v = dg;
                 else if (k < lane && lane < n) v = L[k * LD + lane];
                 a[k] = v;
             }
@@ -1436,8 +1441,16 @@ gpr_wdmma_kernel(VoxelSolveArgs va, int mmax, int mm) {
             continue;
         }
 
-        // ---- L^-1, lane c = column c (rows >= n and columns >= n stay zero)
-        {
+        // ---- L^-1, lane c = column c (rows >= n and columns >= n stay zero);
+        //      NMAX == 16: already in lanes 16..31 (padding columns c >= n
+        //      hold e_c, which meets only zero rows of [f | K*])
+        if constexpr (NMAX == 16) {
+            if (lane >= 16) {
+#pragma unroll
+                for (int r = 0; r < NMAX; ++r) L[r * LD + (lane - 16)] = a[r];
+            }
+            __syncwarp();
+        } else {
             double x[NMAX];
 #pragma unroll
             for (int r = 0; r < NMAX; ++r) {
