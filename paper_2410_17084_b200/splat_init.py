@@ -221,10 +221,9 @@ class _InitQueue:
         items, (camera, image, config) = self.items, self.refs
         self.items, self.ctx, self.refs = [], None, None
         h = init_gaussians_batch([p for p, _ in items], camera, image, config)
-        k = config.n_s * config.n_s
         for i, (pred, lazy) in enumerate(items):
-            lazy._records = {name: v[i * k:(i + 1) * k] for name, v in h.items()}
-            lazy._key = VoxelKey(*(int(v) for v in pred.key))
+            lazy._batch = (h, i)          # records = rows [i k, (i + 1) k) of the batch
+            lazy._key = pred.key
 
 
 _QUEUE = _InitQueue()
@@ -236,13 +235,21 @@ class _LazyPrimitives(list):
 
     def __init__(self, queue, n):
         super().__init__()
-        self._queue, self._n, self._records, self._key = queue, n, None, None
+        self._queue, self._n, self._batch, self._key = queue, n, None, None
+
+    @property
+    def _records(self):
+        if self._batch is None:
+            return None
+        h, i = self._batch
+        k = self._n
+        return {name: v[i * k:(i + 1) * k] for name, v in h.items()}
 
     def _fill(self):
-        if self._records is None:
+        if self._batch is None:
             self._queue.flush()
         if list.__len__(self) == 0 and self._n:
-            h, key = self._records, self._key
+            h, key = self._records, VoxelKey(*(int(v) for v in self._key))
             list.extend(self, [GaussianPrimitive(position=h["position"][i], scale=h["scale"][i],
                                                  rotation=h["rotation"][i],
                                                  opacity=float(h["opacity"][i]),
@@ -250,7 +257,7 @@ class _LazyPrimitives(list):
                                for i in range(self._n)])
 
     def records(self) -> dict:
-        if self._records is None:
+        if self._batch is None:
             self._queue.flush()
         return self._records
 
@@ -304,11 +311,25 @@ class GaussianMap:
         self._lazy = []          # queued _LazyPrimitives (init_gaussians_for_voxel)
 
     def _settle(self):
-        """Append the queued voxels' records (one launch for all of them)."""
+        """Append the queued voxels' records (one launch for all of them); runs
+        of voxels that are consecutive rows of one launch's batch are appended
+        with one copy per field."""
         if self._lazy:
             pend, self._lazy = self._lazy, []
             for lz in pend:
-                self.extend_records(lz.records())
+                if lz._batch is None:
+                    lz.records()                 # flushes the queue: every batch is set
+            j = 0
+            while j < len(pend):
+                h, i0 = pend[j]._batch
+                k = pend[j]._n
+                e = j + 1
+                while e < len(pend) and pend[e]._batch[0] is h and pend[e]._batch[1] == i0 + (e - j) \
+                        and pend[e]._n == k:
+                    e += 1
+                r0, r1 = i0 * k, (i0 + e - j) * k
+                self.extend_records({name: v[r0:r1] for name, v in h.items()})
+                j = e
 
     def _reserve(self, extra: int):
         need = self._n + extra
@@ -345,7 +366,11 @@ class GaussianMap:
     source_keys = property(lambda s: s._get("source_keys"), lambda s, v: s._set("source_keys", v))
 
     def extend(self, primitives: list[GaussianPrimitive]) -> None:
-        if isinstance(primitives, _LazyPrimitives) and primitives._records is None:
+        if isinstance(primitives, _LazyPrimitives) and primitives._batch is None:
+            if self._lazy and self._lazy[-1]._batch is not None:
+                # the queue was flushed since (a new frame's first voxel): settle
+                # the computed voxels now so the queue of lazy objects stays short
+                self._settle()
             self._lazy.append(primitives)        # materialised on the next read
             return
         if not primitives:

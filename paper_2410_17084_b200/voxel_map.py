@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import logging
-from collections.abc import Mapping
+from collections.abc import Mapping, Sequence
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import Iterable, NamedTuple
@@ -121,6 +121,9 @@ class VoxelState(IntEnum):
     CONVERGED = 3
 
 
+_STATES = tuple(VoxelState)          # int -> member without the enum call
+
+
 def voxel_keys(positions: np.ndarray, voxel_size: float) -> np.ndarray:
     """floor(p / voxel_size) as (n, 3) int64, computed by `vx_voxel_keys`."""
     if voxel_size <= 0:
@@ -222,7 +225,7 @@ class FrameUpdateSet:
     @property
     def keys(self) -> list[VoxelKey]:
         if self._keys is None:
-            self._keys = [VoxelKey(int(a), int(b), int(c)) for a, b, c in self.array.tolist()]
+            self._keys = [VoxelKey(a, b, c) for a, b, c in self.array.tolist()]
         return self._keys
 
     def __len__(self) -> int:
@@ -324,6 +327,73 @@ class _Snapshot:
 FRAME_CACHE_MAX = 1 << 17
 
 
+class _EventLog(Sequence):
+    """`VoxelMap.transitions` / `solve_log`: a read-only list whose rows live in
+    numpy chunks (frame, key, old, new) and become `StateTransition` objects
+    (or `(frame, key)` tuples) only when read.  A long-running map therefore
+    holds O(1) Python objects per frame instead of one per transition, which
+    keeps the caller's garbage-collector passes short."""
+
+    def __init__(self, solves: bool = False):
+        self._solves = solves
+        self._chunks = []
+        self._flat = None
+        self._n = 0
+
+    def add(self, frames, keys, old=None, new=None):
+        k = len(frames)
+        if k:
+            self._chunks.append((np.asarray(frames, np.int64), np.asarray(keys, np.int64).reshape(-1, 3),
+                                 None if old is None else np.asarray(old, np.int64),
+                                 None if new is None else np.asarray(new, np.int64)))
+            self._n += k
+            self._flat = None
+
+    def _arrays(self):
+        if self._flat is None:
+            if len(self._chunks) > 1:
+                fr = np.concatenate([c[0] for c in self._chunks])
+                ky = np.concatenate([c[1] for c in self._chunks])
+                od = None if self._solves else np.concatenate([c[2] for c in self._chunks])
+                nw = None if self._solves else np.concatenate([c[3] for c in self._chunks])
+                self._chunks = [(fr, ky, od, nw)]
+            self._flat = self._chunks[0] if self._chunks else \
+                (np.empty(0, np.int64), np.empty((0, 3), np.int64), np.empty(0, np.int64),
+                 np.empty(0, np.int64))
+        return self._flat
+
+    def _rows(self, lo, hi, step=1):
+        fr, ky, od, nw = self._arrays()
+        fr, ky = fr[lo:hi:step].tolist(), ky[lo:hi:step].tolist()
+        if self._solves:
+            return [(f, VoxelKey(*k)) for f, k in zip(fr, ky)]
+        od, nw = od[lo:hi:step].tolist(), nw[lo:hi:step].tolist()
+        return [StateTransition(f, VoxelKey(*k), _STATES[a], _STATES[b])
+                for f, k, a, b in zip(fr, ky, od, nw)]
+
+    def __len__(self):
+        return self._n
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return self._rows(*i.indices(self._n))
+        if i < 0:
+            i += self._n
+        if not 0 <= i < self._n:
+            raise IndexError(i)
+        return self._rows(i, i + 1)[0]
+
+    def __iter__(self):
+        for lo in range(0, self._n, 4096):
+            yield from self._rows(lo, min(lo + 4096, self._n))
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+    def __repr__(self):
+        return f"[{len(self)} {'solves' if self._solves else 'transitions'}]"
+
+
 class _DeviceCell(VoxelCell):
     """A `VoxelCell` backed by the device store.
 
@@ -334,12 +404,13 @@ class _DeviceCell(VoxelCell):
     place) the lazy fields reflect the store when they are first read.
     """
 
-    def __init__(self, vmap, key, vid, state, axis, pred=None):
-        self._vmap, self._vid = vmap, int(vid)
+    def __init__(self, vmap, key, vid, state, axis, pred=None, epoch=None):
+        self._vmap, self._vid = vmap, vid
         self.key = key
-        self.state = VoxelState(int(state))
-        self.value_axis = None if axis < 0 else int(axis)
+        self.state = _STATES[state]
+        self.value_axis = None if axis < 0 else axis
         self._pred = pred            # (positions, colors, variances) or None
+        self._epoch = epoch          # set: the map's frame batch may hold the prediction
         self._lazy = {}
 
     def _fetch(self, name):
@@ -359,7 +430,18 @@ class _DeviceCell(VoxelCell):
 
     @property
     def last_prediction(self):
-        pr = self._pred if self._pred is not None else self._fetch("pred")
+        pr = self._pred
+        if pr is None and self._epoch is not None:
+            # one batched copy serves every touched voxel of the frame
+            found, pr = self._vmap._frame_pred(self._vid, self._epoch)
+            self._epoch = None
+            if found:
+                self._pred = pr
+                self._lazy["pred"] = pr
+        if pr is None and "pred" not in self._lazy:
+            pr = self._fetch("pred")
+        elif pr is None:
+            pr = self._lazy["pred"]
         if pr is None:
             return None
         if not isinstance(pr, VoxelPrediction):
@@ -459,10 +541,13 @@ class VoxelMap:
         self._frame_serial = 0       # bumps when the device frame list changes
         self._snap = None
         self._events = []            # ("t", frame, keys, old, new) / ("s", frame, keys)
-        self._transitions: list[StateTransition] = []
-        self._solve_log: list[tuple[int, VoxelKey]] = []
+        self._transitions = _EventLog()
+        self._solve_log = _EventLog(solves=True)
         self._consumed = 0
         self._solver = None
+        self._fc = None              # frame cache (epoch, {key: entry})
+        self._fp = None              # its batched predictions {vid: tuple}
+        self._fcells = {}            # cells built from it {vid: _DeviceCell}
         self.cells = _CellsView(self)
 
     @classmethod
@@ -513,10 +598,13 @@ class VoxelMap:
 
     # -- per-key cell access (O(touched) traffic) ------------------------------
     def _frame_cache(self):
-        """{key tuple: (vid, state, axis, pred|None)} of the last frame's touched
-        voxels at the current mutation epoch, in one batched device gather."""
-        if getattr(self, "_fc", None) is not None and self._fc[0] == self._epoch:
-            return self._fc[1]
+        """{key tuple: [vid, state, axis, has_pred, cell|None]} of the last frame's
+        touched voxels at the current mutation epoch, in one batched device
+        gather (keys and metadata; the predictions follow on first use, see
+        `_frame_pred`)."""
+        fc = self._fc
+        if fc is not None and fc[0] == self._epoch:
+            return fc[1]
         import torch
         cache = {}
         if self._handle is not None:
@@ -530,51 +618,70 @@ class VoxelMap:
                 st = N.view_tensor(v.state, (V,), np.uint8).index_select(0, vids).long()
                 ax = N.view_tensor(v.value_axis, (V,), np.int8).index_select(0, vids).long()
                 hp = N.view_tensor(v.has_pred, (V,), np.uint8).index_select(0, vids).long()
-                meta = torch.stack([vids, st, ax, hp], 1).cpu().numpy()
-                keys = keys.cpu().numpy()
-                # predictions of the touched voxels that have one (the last
-                # densify's solves among them): one gather, one copy
-                have = np.nonzero(meta[:, 3])[0]
-                preds = {}
-                if len(have):
-                    M = int(v.pred_points)
-                    hv = torch.as_tensor(meta[have, 0], device=vids.device)
-                    slot = N.view_tensor(v.pred_slot, (V,), np.int32).index_select(0, hv).long()
-                    ns = int(slot.max().item()) + 1
-                    px = N.view_tensor(v.pred_xyz, (ns, M, 3), np.float64).index_select(0, slot)
-                    pc = N.view_tensor(v.pred_rgb, (ns, M, 3), np.float64).index_select(0, slot)
-                    pv = N.view_tensor(v.pred_var, (ns, M), np.float64).index_select(0, slot)
-                    px, pc, pv = px.cpu().numpy(), pc.cpu().numpy(), pv.cpu().numpy()
-                    for r, i in enumerate(have):
-                        preds[i] = (px[r], pc[r], pv[r])
-                for i, k in enumerate(keys.tolist()):
-                    cache[tuple(k)] = (int(meta[i, 0]), int(meta[i, 1]), int(meta[i, 2]),
-                                       preds.get(i))
+                meta = torch.cat([torch.stack([vids, st, ax, hp], 1), keys], 1).cpu().tolist()
+                # keyed by plain tuples: equal (and equally hashed) to VoxelKey;
+                # int-only tuple values (the collector untracks them)
+                cache = {(r[4], r[5], r[6]): (r[0], r[1], r[2], r[3]) for r in meta}
         self._fc = (self._epoch, cache)
+        self._fp = None
+        self._fcells = {}
         return cache
 
-    def _cell_for(self, key):
-        k = tuple(int(x) for x in key)
-        if len(k) != 3:
-            raise ValueError("voxel keys have three components")
-        hit = self._frame_cache().get(k)
-        if hit is None:
-            if self._handle is None:
-                return None
+    def _frame_pred(self, vid: int, epoch: int):
+        """(found, prediction tuple | None) of a voxel of the cached frame: the
+        first call at an epoch copies the predictions of every touched voxel
+        that has one in ONE gather (O(touched) bytes)."""
+        fc = self._fc
+        if fc is None or fc[0] != epoch or epoch != self._epoch:
+            return False, None
+        if self._fp is None:
             import torch
-            d = torch.tensor([k], dtype=torch.int64, device=N.device())
-            out = torch.empty(1, dtype=torch.int32, device=d.device)
-            N.check(self._lib.vx_map_lookup(self._h(), N.ptr(d), 1, N.ptr(out), N.stream_ptr()))
-            vid = int(out.item())
-            if vid < 0:
-                return None
-            v = self._view()
-            V = int(v.num_voxels)
-            st = int(N.view_tensor(v.state, (V,), np.uint8)[vid].item())
-            ax = int(N.view_tensor(v.value_axis, (V,), np.int8)[vid].item())
-            hit = (vid, st, ax, None)
-        vid, st, ax, pred = hit
-        return _DeviceCell(self, VoxelKey(*k), vid, st, ax, pred)
+            have = [e[0] for e in fc[1].values() if e[3]]
+            preds = {}
+            if have:
+                v = self._view()
+                V, M = int(v.num_voxels), int(v.pred_points)
+                hv = torch.as_tensor(have, dtype=torch.long, device=N.device())
+                slot = N.view_tensor(v.pred_slot, (V,), np.int32).index_select(0, hv).long()
+                ns = int(slot.max().item()) + 1
+                px = N.view_tensor(v.pred_xyz, (ns, M, 3), np.float64).index_select(0, slot).cpu().numpy()
+                pc = N.view_tensor(v.pred_rgb, (ns, M, 3), np.float64).index_select(0, slot).cpu().numpy()
+                pv = N.view_tensor(v.pred_var, (ns, M), np.float64).index_select(0, slot).cpu().numpy()
+                preds = {h: (px[r], pc[r], pv[r]) for r, h in enumerate(have)}
+            self._fp = preds
+        return True, self._fp.get(vid)
+
+    def _cell_for(self, key):
+        cache = self._frame_cache()
+        hit = cache.get(key) if type(key) in (VoxelKey, tuple) else None
+        if hit is None:
+            k = tuple(int(x) for x in key)
+            if len(k) != 3:
+                raise ValueError("voxel keys have three components")
+            key = VoxelKey(*k)
+            hit = cache.get(k)
+        if hit is not None:
+            c = self._fcells.get(hit[0])
+            if c is None:
+                if type(key) is not VoxelKey:
+                    key = VoxelKey(*key)
+                c = _DeviceCell(self, key, hit[0], hit[1], hit[2], None, self._epoch)
+                self._fcells[hit[0]] = c
+            return c
+        if self._handle is None:
+            return None
+        import torch
+        d = torch.tensor([tuple(key)], dtype=torch.int64, device=N.device())
+        out = torch.empty(1, dtype=torch.int32, device=d.device)
+        N.check(self._lib.vx_map_lookup(self._h(), N.ptr(d), 1, N.ptr(out), N.stream_ptr()))
+        vid = int(out.item())
+        if vid < 0:
+            return None
+        v = self._view()
+        V = int(v.num_voxels)
+        st = int(N.view_tensor(v.state, (V,), np.uint8)[vid].item())
+        ax = int(N.view_tensor(v.value_axis, (V,), np.int8)[vid].item())
+        return _DeviceCell(self, key, vid, st, ax)
 
     def _cell_payload(self, vid: int, want_pred: bool = True) -> dict:
         """raw points (and the prediction) of one voxel: O(voxel) bytes."""
@@ -668,18 +775,25 @@ class VoxelMap:
 
     def _drain_events(self):
         for kind, frame, keys, a, b in self._events[self._consumed:]:
-            for i, k in enumerate(keys.tolist()):
-                key = VoxelKey(*k)
-                if kind == "t":
-                    self._transitions.append(StateTransition(frame, key, VoxelState(int(a[i])),
-                                                             VoxelState(int(b[i]))))
-                else:
-                    self._solve_log.append((frame, key))
-                    # a first solve that converges passes through ACTIVE
-                    for st in range(int(a[i]) + 1, int(b[i]) + 1):
-                        self._transitions.append(StateTransition(
-                            frame, key, VoxelState(st - 1), VoxelState(st)))
+            keys = np.asarray(keys, np.int64).reshape(-1, 3)
+            a, b = np.asarray(a, np.int64), np.asarray(b, np.int64)
+            k = len(keys)
+            if kind == "t":
+                self._transitions.add(np.full(k, frame), keys, a, b)
+            else:
+                self._solve_log.add(np.full(k, frame), keys)
+                # a first solve that converges passes through ACTIVE: solve i adds
+                # the transitions a_i -> a_i + 1 -> ... -> b_i, in solve order
+                cnt = np.maximum(b - a, 0)
+                tot = int(cnt.sum())
+                if tot:
+                    idx = np.repeat(np.arange(k), cnt)
+                    step = np.arange(tot) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+                    old = a[idx] + step
+                    self._transitions.add(np.full(tot, frame), keys[idx], old, old + 1)
         self._consumed = len(self._events)
+        if self._consumed > 64:
+            self._events, self._consumed = [], 0
 
     @property
     def transitions(self) -> list[StateTransition]:
@@ -777,7 +891,8 @@ class VoxelMap:
             N.check(self._lib.vx_map_clear(self._handle, N.stream_ptr()))
         self._mutated()
         self._frame_serial += 1
-        self._events, self._transitions, self._solve_log, self._consumed = [], [], [], 0
+        self._events, self._consumed = [], 0
+        self._transitions, self._solve_log = _EventLog(), _EventLog(solves=True)
 
     # -- audits (voxel_map.py:364-399) --------------------------------------
     def audit_transitions(self) -> list[str]:
