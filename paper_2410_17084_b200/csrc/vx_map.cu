@@ -83,6 +83,8 @@ enum {
     C_F0, C_F1, C_F2, C_F3, C_F4, C_F5, C_F6, C_F7,   // bucket fill cursors
     C_O0, C_O1, C_O2, C_O3, C_O4, C_O5, C_O6, C_O7,   // bucket bases
     C_OK, C_DEGEN, C_CHOL, C_FIRST, C_CONV,
+    C_MAXSEG,         // longest per-voxel run of this frame's points
+    C_BIG,            // runs longer than SEG_WARP_MAX (segment-append big list)
     C_COUNT
 };
 
@@ -155,17 +157,131 @@ __global__ void k_rank_slots(const int32_t* pslot, const int32_t* flags, const i
     tcnt[r] = 0;
 }
 
+// rank of each point's voxel in first-touch order (U: not kept) and an
+// ordinal among the frame's points of that voxel (atomic, arbitrary order:
+// the segment-append kernels restore index order)
 __global__ void k_point_rank(const int32_t* pslot, const int32_t* trank, int64_t n, uint32_t U,
-                             uint32_t* prank, int32_t* tcnt) {
+                             uint32_t* prank, uint32_t* pord, int32_t* tcnt) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int32_t s = pslot[i];
-    uint32_t r = U;
+    uint32_t r = U, o = 0;
     if (s >= 0) {
         r = uint32_t(trank[s]);
-        atomicAdd(tcnt + r, 1);
+        o = uint32_t(atomicAdd(tcnt + r, 1));
     }
     prank[i] = r;
+    if (pord) pord[i] = o;
+}
+
+// counting placement: point i goes to slot tseg[r] + ordinal of its voxel run
+__global__ void k_place(const uint32_t* prank, const uint32_t* pord, int64_t n, uint32_t U,
+                        const int32_t* tseg, uint32_t* sidx) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t r = prank[i];
+    if (r < U) sidx[int64_t(tseg[r]) + pord[i]] = uint32_t(i);
+}
+
+// Segment append (replaces the stable radix sort of (rank, index) pairs and
+// the per-point append): each voxel run of sidx holds its frame indices in
+// arbitrary order; sorting the run restores frame order (voxel_map.py:331-336
+// appends points in frame order), then the run's rows are gathered from the
+// frame and written contiguously to the voxel's arena run.
+constexpr int SEG_WARP_MAX = 512;     // runs a warp sorts in its shared-memory slice
+constexpr int SEG_BIG_MAX = 8192;     // runs a CTA sorts (longer: radix-sort fallback)
+
+__device__ __forceinline__ void seg_copy_rows(const double* __restrict__ xyz,
+                                              const double* __restrict__ rgb, int64_t i,
+                                              int64_t dst, double* axyz, double* argb) {
+    const double x0 = xyz[i * 3], x1 = xyz[i * 3 + 1], x2 = xyz[i * 3 + 2];
+    const double c0 = rgb[i * 3], c1 = rgb[i * 3 + 1], c2 = rgb[i * 3 + 2];
+    axyz[dst * 3] = x0;
+    axyz[dst * 3 + 1] = x1;
+    axyz[dst * 3 + 2] = x2;
+    argb[dst * 3] = c0;
+    argb[dst * 3 + 1] = c1;
+    argb[dst * 3 + 2] = c2;
+}
+
+// bitonic sort of P (power of two) keys in shared memory by `nt` threads
+__device__ __forceinline__ void bitonic_smem(uint32_t* a, int P, int t, int nt, bool warp) {
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int q = t; q < P / 2; q += nt) {
+                const int i = 2 * j * (q / j) + (q % j), l = i + j;
+                const uint32_t x = a[i], y = a[l];
+                const bool asc = (i & k) == 0;
+                if ((x > y) == asc) {
+                    a[i] = y;
+                    a[l] = x;
+                }
+            }
+            if (warp) __syncwarp(); else __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_seg_append_warp(
+        const uint32_t* sidx, const int32_t* tseg, const int32_t* tcnt, int64_t U,
+        const int32_t* tbase, const int32_t* frame_vids, const int64_t* raw_off,
+        const double* __restrict__ xyz, const double* __restrict__ rgb, double* axyz,
+        double* argb, int32_t* big, long long* ctr) {
+    __shared__ uint32_t sm[8][SEG_WARP_MAX];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t* a = sm[w];
+    const int64_t nw = int64_t(gridDim.x) * 8;
+    for (int64_t r = int64_t(blockIdx.x) * 8 + w; r < U; r += nw) {
+        const int L = tcnt[r];
+        if (L <= 0) continue;
+        const int64_t s0 = tseg[r];
+        const int64_t dst = raw_off[frame_vids[r]] + tbase[r];
+        if (L <= 32) {
+            uint32_t v = lane < L ? sidx[s0 + lane] : 0xffffffffu;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    const uint32_t o = __shfl_xor_sync(FULL, v, j);
+                    const bool up = (lane & k) == 0, low = (lane & j) == 0;
+                    v = (low == up) ? (v < o ? v : o) : (v > o ? v : o);
+                }
+            }
+            if (lane < L) seg_copy_rows(xyz, rgb, v, dst + lane, axyz, argb);
+        } else if (L <= SEG_WARP_MAX) {
+            int P = 64;
+            while (P < L) P <<= 1;
+            for (int q = lane; q < P; q += 32) a[q] = q < L ? sidx[s0 + q] : 0xffffffffu;
+            __syncwarp();
+            bitonic_smem(a, P, lane, 32, true);
+            for (int q = lane; q < L; q += 32) seg_copy_rows(xyz, rgb, a[q], dst + q, axyz, argb);
+            __syncwarp();
+        } else if (lane == 0) {
+            big[atomicAdd(reinterpret_cast<unsigned long long*>(ctr + C_BIG), 1ull)] = int32_t(r);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_seg_append_big(
+        const uint32_t* sidx, const int32_t* tseg, const int32_t* tcnt, const int32_t* tbase,
+        const int32_t* frame_vids, const int64_t* raw_off, const double* __restrict__ xyz,
+        const double* __restrict__ rgb, double* axyz, double* argb, const int32_t* big,
+        const long long* ctr) {
+    __shared__ uint32_t a[SEG_BIG_MAX];
+    const long long nbig = ctr[C_BIG];
+    for (long long b = blockIdx.x; b < nbig; b += gridDim.x) {
+        const int r = big[b];
+        const int L = tcnt[r];
+        const int64_t s0 = tseg[r];
+        const int64_t dst = raw_off[frame_vids[r]] + tbase[r];
+        int P = 1024;
+        while (P < L) P <<= 1;
+        for (int q = threadIdx.x; q < P; q += blockDim.x) a[q] = q < L ? sidx[s0 + q] : 0xffffffffu;
+        __syncthreads();
+        bitonic_smem(a, P, threadIdx.x, blockDim.x, false);
+        for (int q = threadIdx.x; q < L; q += blockDim.x) seg_copy_rows(xyz, rgb, a[q], dst + q, axyz, argb);
+        __syncthreads();
+    }
 }
 
 __device__ __forceinline__ int32_t grow_cap(int64_t need) {
@@ -176,7 +292,7 @@ __device__ __forceinline__ int32_t grow_cap(int64_t need) {
 
 __global__ void k_touched_prep(const int32_t* tslot, const int32_t* tcnt, int64_t U,
                                const int32_t* tvals, const int32_t* raw_count, const int32_t* raw_cap,
-                               int32_t* tnew, int64_t* tneed) {
+                               int32_t* tnew, int64_t* tneed, long long* maxseg) {
     const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= U) return;
     const int32_t vid = tvals[tslot[r]];
@@ -186,6 +302,7 @@ __global__ void k_touched_prep(const int32_t* tslot, const int32_t* tcnt, int64_
     const int64_t cap0 = isnew ? 0 : raw_cap[vid];
     const int64_t want = cnt0 + tcnt[r];
     tneed[r] = want > cap0 ? int64_t(grow_cap(want)) : 0;
+    if (tcnt[r] > SEG_WARP_MAX) atomicMax(reinterpret_cast<unsigned long long*>(maxseg), (unsigned long long)tcnt[r]);
 }
 
 struct CommitArgs {
@@ -590,22 +707,23 @@ static int map_store_frame_impl(VxMap* m, const double* xyz, const double* rgb, 
                                          m->fscan.as<int32_t>(), n, m->trank.as<int32_t>(),
                                          m->tslot.as<int32_t>(), m->tcnt.as<int32_t>());
     count_launch();
+    // pord (the per-voxel ordinals) lives in pidx2, the placed runs in pidx and
+    // the big-run list in prank2; the radix fallback below reuses all four
+    uint32_t* pord = m->pidx2.as<uint32_t>();
     k_point_rank<<<nblk(n), 256, 0, s>>>(m->pslot.as<int32_t>(), m->trank.as<int32_t>(), n,
-                                         uint32_t(U), m->prank.as<uint32_t>(), m->tcnt.as<int32_t>());
+                                         uint32_t(U), m->prank.as<uint32_t>(), pord,
+                                         m->tcnt.as<int32_t>());
     count_launch();
     VX_CHECK_LAUNCH();
-    bool in_alt = false;
-    VX_TRY(radix_sort_pairs(m->prank.as<uint32_t>(), m->pidx.as<uint32_t>(), m->prank2.as<uint32_t>(),
-                            m->pidx2.as<uint32_t>(), n, bits_for(U), m->sort_tmp, s, &in_alt,
-                            /*vals_identity=*/true));
-    const uint32_t* srank = in_alt ? m->prank2.as<uint32_t>() : m->prank.as<uint32_t>();
-    const uint32_t* sidx = in_alt ? m->pidx2.as<uint32_t>() : m->pidx.as<uint32_t>();
     VX_TRY(scan_exclusive_i32(m->tcnt.as<int32_t>(), m->tseg.as<int32_t>(), U,
                               reinterpret_cast<int32_t*>(ctr(m) + C_KEPT), m->scan_tmp, s));
     k_touched_prep<<<nblk(U), 256, 0, s>>>(m->tslot.as<int32_t>(), m->tcnt.as<int32_t>(), U,
                                            m->tvals.as<int32_t>(), m->raw_count.as<int32_t>(),
                                            m->raw_cap.as<int32_t>(), m->tnew.as<int32_t>(),
-                                           m->tneed.as<int64_t>());
+                                           m->tneed.as<int64_t>(), ctr(m) + C_MAXSEG);
+    count_launch();
+    k_place<<<nblk(n), 256, 0, s>>>(m->prank.as<uint32_t>(), pord, n, uint32_t(U),
+                                    m->tseg.as<int32_t>(), m->pidx.as<uint32_t>());
     count_launch();
     VX_CHECK_LAUNCH();
     VX_TRY(scan_exclusive_i32(m->tnew.as<int32_t>(), m->tnewscan.as<int32_t>(), U,
@@ -616,6 +734,7 @@ static int map_store_frame_impl(VxMap* m, const double* xyz, const double* rgb, 
     const int64_t n_new = int32_t(m->host_counters[C_NEW] & 0xffffffff);
     const int64_t need = m->host_counters[C_NEED];
     const int64_t kept = int32_t(m->host_counters[C_KEPT] & 0xffffffff);
+    const int64_t maxseg = m->host_counters[C_MAXSEG];
     VX_TRY(ensure_voxels(m, m->num_voxels + n_new, s));
     VX_TRY(ensure_arena(m, m->arena_top + need, s));
 
@@ -634,7 +753,32 @@ static int map_store_frame_impl(VxMap* m, const double* xyz, const double* rgb, 
                                             m->tbase.as<int32_t>(), U, m->raw_off.as<int64_t>(),
                                             m->axyz.as<double>(), m->argb.as<double>());
     count_launch();
-    if (kept > 0) {
+    if (kept > 0 && maxseg <= SEG_BIG_MAX) {
+        // runs restored to frame order per voxel and appended (warp per run;
+        // runs of more than SEG_WARP_MAX points by a CTA each)
+        int64_t wb = (U + 7) / 8;
+        if (wb > int64_t(sm_count()) * 32) wb = int64_t(sm_count()) * 32;
+        k_seg_append_warp<<<unsigned(wb), 256, 0, s>>>(
+            m->pidx.as<uint32_t>(), m->tseg.as<int32_t>(), m->tcnt.as<int32_t>(), U,
+            m->tbase.as<int32_t>(), m->frame_vids.as<int32_t>(), m->raw_off.as<int64_t>(), xyz, rgb,
+            m->axyz.as<double>(), m->argb.as<double>(), m->prank2.as<int32_t>(), ctr(m));
+        count_launch();
+        if (maxseg > SEG_WARP_MAX) {
+            k_seg_append_big<<<unsigned(sm_count() * 2), 1024, 0, s>>>(
+                m->pidx.as<uint32_t>(), m->tseg.as<int32_t>(), m->tcnt.as<int32_t>(),
+                m->tbase.as<int32_t>(), m->frame_vids.as<int32_t>(), m->raw_off.as<int64_t>(), xyz,
+                rgb, m->axyz.as<double>(), m->argb.as<double>(), m->prank2.as<int32_t>(), ctr(m));
+            count_launch();
+        }
+    } else if (kept > 0) {
+        // a run longer than SEG_BIG_MAX points: stable LSD radix sort of
+        // (rank, index) pairs, then the per-point append
+        bool in_alt = false;
+        VX_TRY(radix_sort_pairs(m->prank.as<uint32_t>(), m->pidx.as<uint32_t>(),
+                                m->prank2.as<uint32_t>(), m->pidx2.as<uint32_t>(), n, bits_for(U),
+                                m->sort_tmp, s, &in_alt, /*vals_identity=*/true));
+        const uint32_t* srank = in_alt ? m->prank2.as<uint32_t>() : m->prank.as<uint32_t>();
+        const uint32_t* sidx = in_alt ? m->pidx2.as<uint32_t>() : m->pidx.as<uint32_t>();
         k_append<<<nblk(kept), 256, 0, s>>>(srank, sidx, kept, m->tseg.as<int32_t>(),
                                             m->tbase.as<int32_t>(), m->frame_vids.as<int32_t>(),
                                             m->raw_off.as<int64_t>(), xyz, rgb, m->axyz.as<double>(),

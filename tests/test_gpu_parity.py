@@ -583,3 +583,38 @@ def test_read_ply_matches_reference(name):
     np.testing.assert_array_equal(cloud.positions, ref[name + "_positions"])
     np.testing.assert_array_equal(cloud.colors, ref[name + "_colors"])
     assert np.all(cloud.noise_var == 0.25)
+
+
+@pytest.mark.parametrize("big", [600, 3000, 9000])
+def test_store_frame_runs_of_every_length_keep_frame_order(big):
+    """The segment append (per-voxel runs restored to frame order by a warp
+    register sort <= 32 points, a warp shared-memory sort <= 512, a CTA sort
+    <= 8192, else the radix-sort fallback) against the oracle's store_frame:
+    update order and every voxel's raw point set bit-exact, over two shuffled
+    frames (the second relocates grown runs)."""
+    rng = np.random.default_rng(big)
+    vs = 0.5
+    counts = [1, 5, 31, 32, 33, 100, 511, 512, 513, big]
+    frames = []
+    for f in range(2):
+        pts = []
+        for v, c in enumerate(counts):
+            base = np.array([v * 3 + 0.25, 1.25, -0.75])
+            pts.append(base + rng.uniform(0, 0.49, (c, 3)))
+        pts.append(rng.uniform(-40, 40, (5000, 3)))          # scattered singletons
+        pos = np.concatenate(pts)
+        perm = rng.permutation(len(pos))
+        pos = pos[perm]
+        col = rng.uniform(0, 1, pos.shape)
+        frames.append((pos, col))
+    config = vx.PipelineConfig(voxel_size=vs)
+    omap = O.OracleMap(vs, config.sensor_var, config.tau, config.eta)
+    vmap = vx.VoxelMap.from_config(config)
+    for pos, col in frames:
+        oupd = omap.store_frame(pos, col)
+        upd = vmap.store_frame(vx.PointCloud(pos, col, np.zeros(len(pos))))
+        assert [tuple(k) for k in upd.array.tolist()] == oupd
+    for key, oc in omap.cells.items():
+        c = vmap.cells[key]
+        np.testing.assert_array_equal(c.raw.positions, oc.raw_pos)
+        np.testing.assert_array_equal(c.raw.colors, oc.raw_col)
