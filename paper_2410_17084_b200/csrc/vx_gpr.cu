@@ -1543,15 +1543,30 @@ gpr_wdmma_kernel(VoxelSolveArgs va, int mmax, int mm) {
 
         // ---- nearest training point in the parameter plane (gpr.py:304-305), colours
         int* BI = reinterpret_cast<int*>(base + lay.BI);
-        for (int q = lane; q < m; q += 32) {
-            const double g0 = GC[QRI[q + 1]], g1 = GC[mm + QSI[q + 1]];
-            double best = INFINITY;
-            int bi = 0;
-            for (int i = 0; i < n; ++i) {
-                const double d2 = dist2_exact(g0, g1, X[2 * i], X[2 * i + 1]);
-                if (d2 < best) { best = d2; bi = i; }
+        // three queries per lane in one pass over the training points (each
+        // point's coordinates loaded once, three independent min chains)
+        for (int q0 = lane; q0 < m; q0 += 96) {
+            double g0[3], g1[3], best[3];
+            int bi[3];
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int q = q0 + 32 * u < m ? q0 + 32 * u : q0;
+                g0[u] = GC[QRI[q + 1]];
+                g1[u] = GC[mm + QSI[q + 1]];
+                best[u] = INFINITY;
+                bi[u] = 0;
             }
-            BI[q] = bi;
+            for (int i = 0; i < n; ++i) {
+                const double2 xi = *reinterpret_cast<const double2*>(X + 2 * i);
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const double d2 = dist2_exact(g0[u], g1[u], xi.x, xi.y);
+                    if (d2 < best[u]) { best[u] = d2; bi[u] = i; }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                if (q0 + 32 * u < m) BI[q0 + 32 * u] = bi[u];
         }
         __syncwarp();
         double* COL = base + lay.COL;
