@@ -62,7 +62,10 @@ struct VxMap {
     int64_t* host_counters = nullptr;      // mapped pinned memory (see read_counters)
     int64_t* host_counters_dev = nullptr;  // its device alias
     // temporaries
-    vx::DevBuf scan_tmp, sort_tmp, gpr_work, stage;
+    vx::DevBuf scan_tmp, sort_tmp, gpr_work, gpr_work2, stage;
+    // small frames: the size buckets run concurrently on their own streams
+    cudaStream_t bstream[8] = {};
+    cudaEvent_t bfork = nullptr, bdone[8] = {};
 };
 
 namespace vx {
@@ -522,6 +525,22 @@ __global__ void k_copy_i64(int64_t* __restrict__ dst, const int64_t* __restrict_
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
+constexpr int64_t SMALL_FRAME_CANDIDATES = 65536;
+
+static bool ensure_bucket_streams(VxMap* m) {
+    if (m->bfork) return true;
+    for (int b = 0; b < 8; ++b) {
+        if (cudaStreamCreateWithFlags(&m->bstream[b], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&m->bdone[b], cudaEventDisableTiming) != cudaSuccess)
+            return false;
+    }
+    if (cudaEventCreateWithFlags(&m->bfork, cudaEventDisableTiming) != cudaSuccess) {
+        m->bfork = nullptr;
+        return false;
+    }
+    return true;
+}
+
 static int read_counters(VxMap* m, cudaStream_t s) {
     k_copy_i64<<<1, 64, 0, s>>>(m->host_counters_dev, m->counters.as<int64_t>(), C_COUNT);
     count_launch();
@@ -910,14 +929,30 @@ static int map_densify_impl(VxMap* m, VxDensifyInfo* info, cudaStream_t s) {
                                 NUM_BUCKETS);
     count_launch();
     VX_TRY(launch_bucket_items(a, int(S), m->items.as<int32_t>(), ctr(m) + C_O0, ctr(m) + C_F0, s));
-    // largest buckets first so their tails overlap the small ones
+    // Small frames (one LiDAR scan: a few thousand candidates) are latency-
+    // bound per bucket (each launch lasts at least one voxel of its size), so
+    // the buckets run concurrently on the map's bucket streams, forked from and
+    // joined back into `s`; full-size frames fill the GPU with every bucket and
+    // run them back to back, largest first so their tails overlap.
+    const bool fork = S <= SMALL_FRAME_CANDIDATES && ensure_bucket_streams(m);
+    if (fork) VX_CUDA(cudaEventRecord(m->bfork, s));
     for (int b = NUM_BUCKETS - 1; b >= 0; --b) {
         if (counts[b] == 0) continue;
         a.items = m->items.as<int32_t>() + offs[b];
         a.num_items = int32_t(counts[b]);
-        prof_begin(P_GPR_B0 + b, s);
-        VX_TRY(launch_voxel_solve(a, max_n, m->gpr_work, s, b));
-        prof_end(P_GPR_B0 + b, s);
+        cudaStream_t sb = s;
+        if (fork) {
+            sb = m->bstream[b];
+            VX_CUDA(cudaStreamWaitEvent(sb, m->bfork, 0));
+        }
+        prof_begin(P_GPR_B0 + b, sb);
+        // bucket 7 may take the global-workspace CTA kernel: its own workspace
+        VX_TRY(launch_voxel_solve(a, max_n, b == 7 ? m->gpr_work2 : m->gpr_work, sb, b));
+        prof_end(P_GPR_B0 + b, sb);
+        if (fork) {
+            VX_CUDA(cudaEventRecord(m->bdone[b], sb));
+            VX_CUDA(cudaStreamWaitEvent(s, m->bdone[b], 0));
+        }
     }
     k_dens_finish<<<nblk(S), 256, 0, s>>>(m->cand_status.as<uint8_t>(), m->cand_before.as<uint8_t>(),
                                           m->cand_after.as<uint8_t>(), S, m->okflag.as<int32_t>(),
@@ -1044,8 +1079,13 @@ void map_delete(VxMap* m) {
                       &m->treloc, &m->frame_vids, &m->fb, &m->fa, &m->cflag, &m->cscan,
                       &m->cand_voxel, &m->cand_n, &m->cand_status, &m->cand_before, &m->cand_after,
                       &m->items, &m->okflag, &m->okscan, &m->solved_vids, &m->cand_axis, &m->cand_meanf, &m->counters, &m->scan_tmp,
-                      &m->sort_tmp, &m->gpr_work, &m->stage};
+                      &m->sort_tmp, &m->gpr_work, &m->gpr_work2, &m->stage};
     for (DevBuf* b : bufs) b->release();
+    for (int b = 0; b < 8; ++b) {
+        if (m->bstream[b]) cudaStreamDestroy(m->bstream[b]);
+        if (m->bdone[b]) cudaEventDestroy(m->bdone[b]);
+    }
+    if (m->bfork) cudaEventDestroy(m->bfork);
     if (m->host_counters) cudaFreeHost(m->host_counters);
     delete m;
 }
