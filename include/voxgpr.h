@@ -268,7 +268,11 @@ int vx_map_init_gaussians(VxMap* map, const int32_t* d_voxels, int64_t count,
 
 /* One ingest (pipeline.py:139-171 with expansion_threshold = 1): store,
  * densify, then Gaussians for first solves into `out` (capacity in records).
- * *out_records = records written.  camera/image may be NULL (no init). */
+ * *out_records = records written.  camera/image may be NULL (no init).
+ * camera set and out NULL: the records are deferred - the first-solve list is
+ * kept, *out_records = the records it needs, and vx_map_emit_first_gaussians
+ * writes them (a caller can stage the frame's image while the frame is
+ * stored and solved). */
 int vx_map_ingest(VxMap* map, const double* d_xyz, const double* d_rgb, int64_t n,
                   const VxCamera* camera, const double* d_image, const VxSplatConfig* cfg,
                   VxGaussianOut* out, int64_t out_capacity, int64_t* out_records,

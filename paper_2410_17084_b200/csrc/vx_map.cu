@@ -989,7 +989,8 @@ int map_ingest(VxMap* m, const double* xyz, const double* rgb, int64_t n, const 
     VX_TRY(map_store_frame(m, xyz, rgb, n, fi, s));
     VX_TRY(map_densify(m, &dloc, s));
     if (di) *di = dloc;
-    if (cam == nullptr || out == nullptr || dloc.first_solves == 0) return VX_OK;
+    m->first_count = 0;
+    if (cam == nullptr || dloc.first_solves == 0) return VX_OK;
     const int64_t S = m->solve_candidates;
     // first solves in update order: status OK and READY before (pipeline.py:145-156)
     k_first_solves<<<nblk(S), 256, 0, s>>>(m->cand_voxel.as<int32_t>(), m->cand_status.as<uint8_t>(),
@@ -1005,6 +1006,12 @@ int map_ingest(VxMap* m, const double* xyz, const double* rgb, int64_t n, const 
     count_launch();
     VX_CHECK_LAUNCH();
     m->first_count = dloc.first_solves;
+    if (out == nullptr) {
+        // deferred: the first-solve list is kept for vx_map_emit_first_gaussians
+        // (the caller stages the image while the frame is solved)
+        if (out_records) *out_records = m->first_count * scfg->n_s * scfg->n_s;
+        return VX_OK;
+    }
     return map_emit_first_gaussians(m, cam, image, scfg, out, out_capacity, out_records, s);
 }
 

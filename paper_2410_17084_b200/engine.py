@@ -83,8 +83,8 @@ class MappingEngine:
         # device-wide: the old buffer may still be read by a D2H on another stream
         torch.cuda.synchronize()
 
-    def _stage(self, name, arr):
-        """Copy a host array into a reusable pinned buffer, then H2D (async)."""
+    def _stage_host(self, name, arr):
+        """Copy a host array into a reusable pinned buffer (no device work)."""
         import torch
         a = np.ascontiguousarray(arr, dtype=np.float64)
         buf = self._pinned.get(name)
@@ -93,7 +93,11 @@ class MappingEngine:
             self._pinned[name] = buf
         host = buf[:a.size]
         host.numpy()[:] = a.reshape(-1)
-        return host.view(*a.shape).to(N.device(), non_blocking=True)
+        return host.view(*a.shape)
+
+    def _stage(self, name, arr):
+        """Copy a host array into a reusable pinned buffer, then H2D (async)."""
+        return self._stage_host(name, arr).to(N.device(), non_blocking=True)
 
     def _first_solves(self, frame_index: int):
         """(voxel ids, order keys) of the last densify's first solves, update order."""
@@ -156,12 +160,29 @@ class MappingEngine:
 
     # -- ingest -------------------------------------------------------------
     def ingest(self, positions, colors, camera=None, image=None) -> IngestReport:
-        """Host-array ingest: H2D of the scan (and image), then `ingest_device`."""
+        """Host-array ingest: H2D of the scan (and image), then `ingest_device`.
+
+        The image (7 MB for a 640x480 float64 frame) is copied into its pinned
+        buffer on a helper thread while the device stores and solves the scan;
+        its H2D is issued, and the Gaussians emitted, once the copy is done."""
         t0 = time.perf_counter()
+        deferred = image is not None and camera is not None and self.config.expansion_threshold <= 1
+        fut = None
+        if deferred:
+            if getattr(self, "_stager", None) is None:
+                from concurrent.futures import ThreadPoolExecutor
+                self._stager = ThreadPoolExecutor(max_workers=1, thread_name_prefix="vx-stage")
+            ev = getattr(self, "_img_ev", None)
+            if ev is not None:
+                ev.synchronize()            # the last frame's image H2D has left the pinned buffer
+            fut = self._stager.submit(self._stage_host, "img", image)
         dx = self._stage("xyz", positions) if len(positions) else None
         dc = self._stage("rgb", colors) if len(positions) else None
-        di = self._stage("img", image) if image is not None else None
-        rep = self.ingest_device(dx, dc, len(positions), camera, di)
+        if deferred:
+            rep = self.ingest_device(dx, dc, len(positions), camera, None, image_future=fut)
+        else:
+            di = self._stage("img", image) if image is not None else None
+            rep = self.ingest_device(dx, dc, len(positions), camera, di)
         rep.duration_s = time.perf_counter() - t0
         return rep
 
@@ -304,7 +325,8 @@ class MappingEngine:
         drain(0)
         return reports
 
-    def ingest_device(self, d_xyz, d_rgb, n: int, camera=None, d_image=None) -> IngestReport:
+    def ingest_device(self, d_xyz, d_rgb, n: int, camera=None, d_image=None,
+                      image_future=None) -> IngestReport:
         t0 = time.perf_counter()
         cfg = self.config
         vm = self.vmap
@@ -327,12 +349,27 @@ class MappingEngine:
                 cfg.n_s, cfg.n_r, cfg.weight_floor, cfg.scale_floor, cfg.initial_opacity,
                 cfg.rotation)
             written = C.c_int64(0)
-            rc = lib.vx_map_ingest(vm._h(), N.ptr(d_xyz), N.ptr(d_rgb), int(n), C.byref(cam),
-                                   N.ptr(d_image), C.byref(sc), C.byref(out),
-                                   self.records.count - self.num_gaussians, C.byref(written),
-                                   C.byref(fi), C.byref(di), N.stream_ptr())
-            vm._mutated()
-            vm._frame_serial += 1
+            if image_future is not None:
+                # records deferred until the image (staged on the helper thread
+                # meanwhile) is on the device
+                rc = lib.vx_map_ingest(vm._h(), N.ptr(d_xyz), N.ptr(d_rgb), int(n), C.byref(cam),
+                                       N.ptr(None), C.byref(sc), None, 0, C.byref(written),
+                                       C.byref(fi), C.byref(di), N.stream_ptr())
+                vm._mutated()
+                vm._frame_serial += 1
+                import torch
+                d_image = image_future.result().to(N.device(), non_blocking=True)
+                self._img_ev = torch.cuda.Event()
+                self._img_ev.record()
+                if rc == N.VX_OK and written.value:
+                    rc = N.VX_E_CAPACITY           # emit below (grows the buffer if needed)
+            else:
+                rc = lib.vx_map_ingest(vm._h(), N.ptr(d_xyz), N.ptr(d_rgb), int(n), C.byref(cam),
+                                       N.ptr(d_image), C.byref(sc), C.byref(out),
+                                       self.records.count - self.num_gaussians, C.byref(written),
+                                       C.byref(fi), C.byref(di), N.stream_ptr())
+                vm._mutated()
+                vm._frame_serial += 1
             if rc == N.VX_E_CAPACITY:
                 # the frame is stored and densified; its first-solve list is kept
                 # by the library until the next mutating call
