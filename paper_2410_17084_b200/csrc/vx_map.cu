@@ -529,6 +529,7 @@ constexpr int64_t SMALL_FRAME_CANDIDATES = 65536;
 
 static bool ensure_bucket_streams(VxMap* m) {
     if (m->bfork) return true;
+    if (m->bstream[0]) return false;      // an earlier attempt failed part-way: stay serial
     for (int b = 0; b < 8; ++b) {
         if (cudaStreamCreateWithFlags(&m->bstream[b], cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&m->bdone[b], cudaEventDisableTiming) != cudaSuccess)

@@ -20,7 +20,7 @@ import numpy as np
 from . import _native as N
 from .config import PipelineConfig
 from .formats import PlyPayload
-from .splat_init import GaussianMap, GaussianRecords
+from .splat_init import GaussianMap, GaussianRecords, image_for_camera
 from .voxel_map import VoxelMap
 
 
@@ -166,6 +166,8 @@ class MappingEngine:
         buffer on a helper thread while the device stores and solves the scan;
         its H2D is issued, and the Gaussians emitted, once the copy is done."""
         t0 = time.perf_counter()
+        if image is not None and camera is not None:
+            image = image_for_camera(camera, image)
         deferred = image is not None and camera is not None and self.config.expansion_threshold <= 1
         fut = None
         if deferred:
@@ -246,6 +248,8 @@ class MappingEngine:
                                                       N.ptr(b["rgb"]), N.vp(copier.cuda_stream)),
                                 f"vx_decode_ply {pos.path}")
                     pos = b["xyz"]
+                if img is not None and cam is not None:
+                    img = image_for_camera(cam, img)
                 for name, t in (("xyz", pos), ("rgb", col), ("img", img)):
                     if decoded and name != "img":
                         continue          # decoded in place above
@@ -328,6 +332,8 @@ class MappingEngine:
     def ingest_device(self, d_xyz, d_rgb, n: int, camera=None, d_image=None,
                       image_future=None) -> IngestReport:
         t0 = time.perf_counter()
+        if d_image is not None and camera is not None:
+            d_image = image_for_camera(camera, d_image)
         cfg = self.config
         vm = self.vmap
         vm._h()

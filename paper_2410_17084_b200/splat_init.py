@@ -119,7 +119,7 @@ def init_color(position: np.ndarray, camera: Camera, image: np.ndarray,
     lib = N.lib()
     dp = N.to_device(np.asarray(position, dtype=float).reshape(1, 3))
     df = N.to_device(np.asarray(fallback_rgb, dtype=float).reshape(1, 3))
-    di = N.to_device(np.asarray(image, dtype=float))
+    di = N.to_device(image_for_camera(camera, np.asarray(image, dtype=float)))
     out = torch.empty((1, 3), dtype=torch.float64, device=dp.device)
     cam = N.camera_struct(camera)
     N.check(lib.vx_init_color(N.ptr(dp), N.ptr(df), 1, C.byref(cam), N.ptr(di), N.ptr(out),
@@ -162,6 +162,27 @@ class GaussianRecords:
                 ("position", "scale", "rotation", "opacity", "color", "source_key")}
 
 
+def image_for_camera(camera, image):
+    """The (height, width, 3) pixel block the device samples (init_color,
+    splat_init.py:124-130 indexes image[iv, iu] for iv < height, iu < width).
+
+    A larger image is cropped to that block (the same pixels the reference
+    reads); one that does not cover the camera raises IndexError up front (the
+    reference would raise it when a Gaussian projects onto a missing pixel),
+    since the device reads the block without per-pixel bounds.  numpy arrays
+    come back as contiguous float64, torch tensors as contiguous tensors."""
+    H, W = int(camera.height), int(camera.width)
+    shape = tuple(image.shape)
+    if len(shape) != 3 or shape[0] < H or shape[1] < W or shape[2] < 3:
+        raise IndexError(f"image of shape {shape} does not cover the camera's {H}x{W} pixels "
+                         f"(expected ({H}, {W}, 3))")
+    if shape != (H, W, 3):
+        image = image[:H, :W, :3]
+    if hasattr(image, "contiguous"):
+        return image.contiguous()
+    return np.ascontiguousarray(image, dtype=np.float64)
+
+
 def init_gaussians_batch(predictions, camera: Camera, image: np.ndarray, config) -> dict:
     """Gaussian records of many predictions in one launch (host SoA dict)."""
     lib = N.lib()
@@ -179,7 +200,7 @@ def init_gaussians_batch(predictions, camera: Camera, image: np.ndarray, config)
     dc = N.to_device(np.stack([p.colors for p in preds]))
     dv = N.to_device(np.stack([p.variances for p in preds]))
     dk = N.to_device(np.array([tuple(p.key) for p in preds], dtype=np.int64), np.int64)
-    di = N.to_device(np.asarray(image, dtype=float))
+    di = N.to_device(image_for_camera(camera, np.asarray(image, dtype=float)))
     recs = GaussianRecords(len(preds) * config.n_s * config.n_s)
     cam, sc, out = N.camera_struct(camera), _splat_cfg(config), recs.out_struct()
     N.check(lib.vx_gaussians_from_predictions(N.ptr(dx), N.ptr(dc), N.ptr(dv), N.ptr(dk),

@@ -134,3 +134,25 @@ def test_renderer_host_helpers_match_reference_semantics():
         from paper_2410_17084_b200 import _native as N
         with pytest.raises(N.NativeUnavailable):
             R.render([], vx.Camera(fx=1, fy=1, cx=0, cy=0, width=4, height=4))
+
+
+def test_image_for_camera_crops_and_rejects():
+    """The device samples a (height, width, 3) float64 block: larger images are
+    cropped to the pixels the reference indexes, smaller ones raise IndexError
+    before any device read (no CPU fallback is involved: host validation only)."""
+    import numpy as np
+    from paper_2410_17084_b200.camera import Camera
+    from paper_2410_17084_b200.splat_init import image_for_camera
+    cam = Camera(fx=10.0, fy=10.0, cx=3.5, cy=2.5, width=8, height=6)
+    img = np.arange(7 * 9 * 4, dtype=float).reshape(7, 9, 4)
+    out = image_for_camera(cam, img)
+    assert out.shape == (6, 8, 3) and out.flags.c_contiguous
+    np.testing.assert_array_equal(out, img[:6, :8, :3])
+    exact = np.zeros((6, 8, 3))
+    assert image_for_camera(cam, exact) is exact
+    for bad in (np.zeros((5, 8, 3)), np.zeros((6, 7, 3)), np.zeros((6, 8)), np.zeros((6, 8, 2))):
+        try:
+            image_for_camera(cam, bad)
+        except IndexError:
+            continue
+        raise AssertionError(f"shape {bad.shape} accepted")
