@@ -145,7 +145,7 @@ def test_large_n_panel_kernel_team_sizes(c, monkeypatch):
     monkeypatch.setenv("VX_PANEL_C", str(c))
     rng = np.random.default_rng(77)
     probs = []
-    for n, m in ((161, 81), (300, 256), (742, 81), (190, 7), (450, 81)):
+    for n, m in ((161, 81), (300, 256), (742, 81), (190, 7), (450, 81), (2000, 81)):
         x = rng.uniform(0, 0.5, (n, 2))
         f = rng.normal(0, 0.05, n)
         nz = rng.uniform(1e-4, 1e-2, n)
