@@ -175,7 +175,7 @@ class VoxelPrediction:
         return float(self.variances.mean())
 
 
-@dataclass
+@dataclass(slots=True)
 class VoxelCell:
     key: VoxelKey
     raw: PointCloud = field(default_factory=PointCloud.empty)
@@ -401,8 +401,12 @@ class _DeviceCell(VoxelCell):
     and `last_prediction` are copied from HBM on first access (only this
     voxel's rows), or come from the batch the map prefetched for the last
     frame's solved voxels.  Like the reference's cells (which the map mutates in
-    place) the lazy fields reflect the store when they are first read.
+    place) the lazy fields reflect the store when they are first read.  Slotted,
+    with the lazy-field dict made on first use: a frame's thousands of cells
+    are one tracked object each for the caller's garbage collector.
     """
+
+    __slots__ = ("_vmap", "_vid", "_pred", "_epoch", "_lazy")
 
     def __init__(self, vmap, key, vid, state, axis, pred=None, epoch=None):
         self._vmap, self._vid = vmap, vid
@@ -411,14 +415,20 @@ class _DeviceCell(VoxelCell):
         self.value_axis = None if axis < 0 else axis
         self._pred = pred            # (positions, colors, variances) or None
         self._epoch = epoch          # set: the map's frame batch may hold the prediction
-        self._lazy = {}
+        self._lazy = None
+
+    def _lz(self) -> dict:
+        if self._lazy is None:
+            self._lazy = {}
+        return self._lazy
 
     def _fetch(self, name):
-        if name not in self._lazy:
-            self._lazy.update(self._vmap._cell_payload(self._vid, want_pred=self._pred is None))
+        lz = self._lz()
+        if name not in lz:
+            lz.update(self._vmap._cell_payload(self._vid, want_pred=self._pred is None))
             if self._pred is not None:
-                self._lazy["pred"] = self._pred
-        return self._lazy[name]
+                lz["pred"] = self._pred
+        return lz[name]
 
     @property
     def raw(self):
@@ -426,7 +436,7 @@ class _DeviceCell(VoxelCell):
 
     @raw.setter
     def raw(self, v):
-        self._lazy["raw"] = v
+        self._lz()["raw"] = v
 
     @property
     def last_prediction(self):
@@ -437,34 +447,34 @@ class _DeviceCell(VoxelCell):
             self._epoch = None
             if found:
                 self._pred = pr
-                self._lazy["pred"] = pr
-        if pr is None and "pred" not in self._lazy:
-            pr = self._fetch("pred")
-        elif pr is None:
-            pr = self._lazy["pred"]
+                self._lz()["pred"] = pr
+        if pr is None:
+            lz = self._lz()
+            pr = lz["pred"] if "pred" in lz else self._fetch("pred")
         if pr is None:
             return None
         if not isinstance(pr, VoxelPrediction):
             pr = VoxelPrediction(self.key, *pr)
             self._pred = pr
-            self._lazy["pred"] = pr
+            self._lz()["pred"] = pr
         return pr
 
     @last_prediction.setter
     def last_prediction(self, v):
         self._pred = v
-        self._lazy["pred"] = v
+        self._lz()["pred"] = v
 
     @property
     def pseudo(self):
-        if "pseudo" in self._lazy:
-            return self._lazy["pseudo"]
+        lz = self._lz()
+        if "pseudo" in lz:
+            return lz["pseudo"]
         pr = self.last_prediction
         return None if pr is None else PointCloud(pr.positions, pr.colors, pr.variances)
 
     @pseudo.setter
     def pseudo(self, v):
-        self._lazy["pseudo"] = v
+        self._lz()["pseudo"] = v
 
 
 class _CellsView(Mapping):
@@ -481,7 +491,15 @@ class _CellsView(Mapping):
         self._m = vmap
 
     def __getitem__(self, key):
-        c = self._m._cell_for(key)
+        m = self._m
+        fc = m._fc
+        if fc is not None and fc[0] == m._epoch and type(key) in (VoxelKey, tuple):
+            hit = fc[1].get(key)           # a cell already built at this epoch
+            if hit is not None:
+                c = m._fcells.get(hit[0])
+                if c is not None:
+                    return c
+        c = m._cell_for(key)
         if c is None:
             raise KeyError(key)
         return c
