@@ -254,6 +254,8 @@ class _LazyPrimitives(list):
     """The n_s^2 primitives of one queued voxel: a list that fills itself from
     the coalesced launch on first read (length known up front)."""
 
+    __slots__ = ("_queue", "_n", "_batch", "_key")
+
     def __init__(self, queue, n):
         super().__init__()
         self._queue, self._n, self._batch, self._key = queue, n, None, None

@@ -51,7 +51,7 @@ class ColoredPoint:
             raise InputDomainError("noise_var must be nonnegative")
 
 
-@dataclass
+@dataclass(slots=True)
 class PointCloud:
     """Struct-of-arrays batch of colored points (host arrays, validated)."""
 
@@ -160,7 +160,7 @@ def voxel_bounds(key, voxel_size: float) -> np.ndarray:
 # Cells, predictions, frame bookkeeping (voxel_map.py:156-221)
 # ---------------------------------------------------------------------------
 
-@dataclass
+@dataclass(slots=True)
 class VoxelPrediction:
     key: VoxelKey
     positions: np.ndarray
@@ -243,7 +243,7 @@ class FrameUpdateSet:
         return f"FrameUpdateSet({len(self)} keys)"
 
 
-@dataclass
+@dataclass(slots=True)
 class StateTransition:
     frame: int
     key: VoxelKey
