@@ -494,11 +494,14 @@ class _CellsView(Mapping):
         m = self._m
         fc = m._fc
         if fc is not None and fc[0] == m._epoch and type(key) in (VoxelKey, tuple):
-            hit = fc[1].get(key)           # a cell already built at this epoch
+            hit = fc[1].get(key)           # a touched voxel of the cached frame
             if hit is not None:
                 c = m._fcells.get(hit[0])
-                if c is not None:
-                    return c
+                if c is None:
+                    c = _DeviceCell(m, key if type(key) is VoxelKey else VoxelKey(*key), hit[0],
+                                    hit[1], hit[2], None, fc[0])
+                    m._fcells[hit[0]] = c
+                return c
         c = m._cell_for(key)
         if c is None:
             raise KeyError(key)
@@ -565,6 +568,7 @@ class VoxelMap:
         self._solver = None
         self._fc = None              # frame cache (epoch, {key: entry})
         self._fp = None              # its batched predictions {vid: tuple}
+        self._fp_rest = True         # touched voxels not yet in _fp may still be fetched
         self._fcells = {}            # cells built from it {vid: _DeviceCell}
         self.cells = _CellsView(self)
 
@@ -646,28 +650,50 @@ class VoxelMap:
         return cache
 
     def _frame_pred(self, vid: int, epoch: int):
-        """(found, prediction tuple | None) of a voxel of the cached frame: the
-        first call at an epoch copies the predictions of every touched voxel
-        that has one in ONE gather (O(touched) bytes)."""
+        """(found, prediction tuple | None) of a voxel of the cached frame.
+
+        Predictions arrive in batched gathers (O(touched) bytes): the first
+        request at an epoch fetches the last densify's first solves among the
+        touched voxels (what the pipeline's expansion loop reads,
+        pipeline.py:160-165); a request outside that batch fetches every other
+        touched voxel that has a prediction."""
         fc = self._fc
         if fc is None or fc[0] != epoch or epoch != self._epoch:
             return False, None
         if self._fp is None:
-            import torch
-            have = [e[0] for e in fc[1].values() if e[3]]
-            preds = {}
-            if have:
-                v = self._view()
-                V, M = int(v.num_voxels), int(v.pred_points)
-                hv = torch.as_tensor(have, dtype=torch.long, device=N.device())
-                slot = N.view_tensor(v.pred_slot, (V,), np.int32).index_select(0, hv).long()
-                ns = int(slot.max().item()) + 1
-                px = N.view_tensor(v.pred_xyz, (ns, M, 3), np.float64).index_select(0, slot).cpu().numpy()
-                pc = N.view_tensor(v.pred_rgb, (ns, M, 3), np.float64).index_select(0, slot).cpu().numpy()
-                pv = N.view_tensor(v.pred_var, (ns, M), np.float64).index_select(0, slot).cpu().numpy()
-                preds = {h: (px[r], pc[r], pv[r]) for r, h in enumerate(have)}
-            self._fp = preds
+            self._fp, self._fp_rest = {}, True
+            first = self._last_first_solves()
+            if first:
+                self._fetch_preds([e[0] for e in fc[1].values() if e[3] and e[0] in first])
+        if vid not in self._fp and self._fp_rest:
+            self._fp_rest = False
+            self._fetch_preds([e[0] for e in fc[1].values() if e[3] and e[0] not in self._fp])
         return True, self._fp.get(vid)
+
+    def _last_first_solves(self) -> set:
+        """Voxel ids the last densify solved for the first time (READY before)."""
+        v = self._view()
+        S = int(v.solve_candidates)
+        if not S:
+            return set()
+        st = N.view_tensor(v.solve_status, (S,), np.uint8)
+        bf = N.view_tensor(v.solve_state_before, (S,), np.uint8)
+        vids = N.view_tensor(v.solve_voxels, (S,), np.int32)
+        return set(vids[(st == N.ST_OK) & (bf == int(VoxelState.READY))].cpu().tolist())
+
+    def _fetch_preds(self, vids: list):
+        if not vids:
+            return
+        import torch
+        v = self._view()
+        V, M = int(v.num_voxels), int(v.pred_points)
+        hv = torch.as_tensor(vids, dtype=torch.long, device=N.device())
+        slot = N.view_tensor(v.pred_slot, (V,), np.int32).index_select(0, hv).long()
+        ns = int(slot.max().item()) + 1
+        px = N.view_tensor(v.pred_xyz, (ns, M, 3), np.float64).index_select(0, slot).cpu().numpy()
+        pc = N.view_tensor(v.pred_rgb, (ns, M, 3), np.float64).index_select(0, slot).cpu().numpy()
+        pv = N.view_tensor(v.pred_var, (ns, M), np.float64).index_select(0, slot).cpu().numpy()
+        self._fp.update({h: (px[r], pc[r], pv[r]) for r, h in enumerate(vids)})
 
     def _cell_for(self, key):
         cache = self._frame_cache()

@@ -32,3 +32,29 @@ for i, (pos, col) in enumerate(frames):
     t6 = time.perf_counter()
     print(f"frame {i}: store {1e3*(t1-t0):6.1f}  state-scan {1e3*(t2-t1):6.1f} ({len(up)} keys)  "
           f"densify {1e3*(t3-t2):6.1f} ({len(preds)} solved)  cells {1e3*(t4-t3):6.1f}  engine {1e3*(t6-t5):6.1f}")
+
+# expansion loop of pipeline.py:154-171 on the last frame's first solves
+import gc
+gc.disable()
+cam = vx.Camera(100.0, 100.0, 79.5, 59.5, 160, 120)
+img = np.zeros((120, 160, 3))
+gm = vx.GaussianMap()
+pos, col = scenes.config1_scan(seed=0, frame=12, rays=60000)
+up = vmap.store_frame(vx.PointCloud(pos, col, np.zeros(len(pos))))
+t0 = time.perf_counter()
+first = {k for k in up if vmap.cells[k].state == vx.VoxelState.READY}
+t1 = time.perf_counter()
+preds = vx.densify_frame(up, vmap, cfg)
+t2 = time.perf_counter()
+newly = [p.key for p in preds if p.key in first]
+n = 0
+for key in newly:
+    cell = vmap.cells[key]
+    prims = vx.init_gaussians_for_voxel(cell.last_prediction, cam, img, cfg)
+    gm.extend(prims)
+    n += len(prims)
+t3 = time.perf_counter()
+_ = gm.positions
+t4 = time.perf_counter()
+print(f"gc off: state-scan {1e3*(t1-t0):.1f} ({len(up)} keys)  densify {1e3*(t2-t1):.1f} ({len(preds)})  "
+      f"expansion {1e3*(t3-t2):.1f} ({len(newly)} voxels, {n} prims)  settle {1e3*(t4-t3):.1f}")
