@@ -254,6 +254,20 @@ int vx_map_view(VxMap* map, VxMapView* out);
 int vx_map_store_frame(VxMap* map, const double* d_xyz, const double* d_rgb, int64_t n,
                        VxFrameInfo* info, void* stream);
 
+/* Input slicing for sharded maps (B200 extension): this rank
+ * holds rows [global_base, global_base + n) of a scan; group them by the rank
+ * that owns their voxel (mix64(key) % shard_world, the owner test of
+ * vx_map_store_frame; points without a valid key go to rank 0, which reports
+ * them).  d_out_xyz / d_out_rgb (n, 3) and d_out_index (n, global row numbers)
+ * receive the rows grouped by owner, frame order kept within each group;
+ * h_counts (HOST int64[shard_world + 1]) the group sizes, then the number of
+ * rows without a valid key (already counted in rank 0's group).  After an all-to-all
+ * by these counts every rank holds its voxels' points in global frame order
+ * (concatenated by source rank) for vx_map_store_frame / vx_map_ingest. */
+int vx_map_partition_by_owner(VxMap* map, const double* d_xyz, const double* d_rgb, int64_t n,
+                              int64_t global_base, double* d_out_xyz, double* d_out_rgb,
+                              int64_t* d_out_index, int64_t* h_counts, void* stream);
+
 /* densify_frame (gpr.py:269-311) on the last frame's touched voxels: PCA
  * value axis, grid, SE Cholesky posterior, nearest colour, clip, and
  * apply_prediction (voxel_map.py:242-261,344-355).  Statuses / states in

@@ -120,6 +120,7 @@ _SIGS = {
     "vx_map_emit_first_gaussians": ([vp, C.POINTER(VxCamera), vp, C.POINTER(VxSplatConfig),
                                      C.POINTER(VxGaussianOut), C.c_int64, c_i64p, vp], C.c_int),
     "vx_map_lookup": ([vp, vp, C.c_int64, vp, vp], C.c_int),
+    "vx_map_partition_by_owner": ([vp, vp, vp, C.c_int64, C.c_int64, vp, vp, vp, c_i64p, vp], C.c_int),
     "vx_map_set_frame_keys": ([vp, vp, C.c_int64, vp], C.c_int),
     "vx_map_apply_prediction": ([vp, c_i64p, vp, vp, vp, C.c_int64, C.POINTER(C.c_uint8), vp],
                                 C.c_int),

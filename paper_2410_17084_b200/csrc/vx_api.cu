@@ -451,6 +451,17 @@ int vx_map_store_frame(VxMap* map, const double* d_xyz, const double* d_rgb, int
     return map_store_frame(map, d_xyz, d_rgb, n, info, as_stream(stream));
 }
 
+int vx_map_partition_by_owner(VxMap* map, const double* d_xyz, const double* d_rgb, int64_t n,
+                              int64_t global_base, double* d_out_xyz, double* d_out_rgb,
+                              int64_t* d_out_index, int64_t* h_counts, void* stream) {
+    if (!map || !h_counts || (n > 0 && (!d_xyz || !d_rgb || !d_out_xyz || !d_out_rgb || !d_out_index))) {
+        set_error("null argument");
+        return VX_E_INPUT;
+    }
+    return map_partition_by_owner(map, d_xyz, d_rgb, n, global_base, d_out_xyz, d_out_rgb,
+                                  d_out_index, h_counts, as_stream(stream));
+}
+
 int vx_map_densify(VxMap* map, VxDensifyInfo* info, void* stream) {
     if (!map) {
         set_error("null map");

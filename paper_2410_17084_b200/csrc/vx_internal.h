@@ -61,6 +61,9 @@ int scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tota
                        DevBuf& tmp, cudaStream_t s);
 // stable LSD radix sort of (key, value) pairs by the low `bits` bits of key;
 // vals_identity: the values are 0..n-1, generated instead of read
+int map_partition_by_owner(VxMap* m, const double* xyz, const double* rgb, int64_t n,
+                           int64_t gbase, double* oxyz, double* orgb, int64_t* ogidx,
+                           int64_t* h_counts, cudaStream_t s);
 int radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
                      int64_t n, int bits, DevBuf& tmp, cudaStream_t s, bool* result_in_alt,
                      bool vals_identity = false);

@@ -626,6 +626,95 @@ static int bits_for(int64_t v) {
     return b;
 }
 
+// ------------------------------------------------------------------ input slicing (N > 1)
+// A rank holding a slice of a scan sends each point to the rank that owns its
+// voxel.  Owner = shard_of(key) exactly as k_hash_points computes it; a point
+// whose key cannot be formed (non-finite, outside the lattice) goes to rank 0,
+// whose hashing kernel then reports it.  Per-CTA owner histograms feed the
+// world counters with one atomic per owner and CTA.
+__global__ void k_owner_of_points(const double* __restrict__ xyz, int64_t n, double vs, int world,
+                                  uint32_t* owner, unsigned long long* counts) {
+    __shared__ unsigned int h[65];
+    for (int w = threadIdx.x; w <= world; w += blockDim.x) h[w] = 0;
+    __syncthreads();
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double x = xyz[i * 3], y = xyz[i * 3 + 1], z = xyz[i * 3 + 2];
+        uint32_t o = 0;
+        bool valid = false;
+        if (isfinite(x) && isfinite(y) && isfinite(z)) {
+            const double fx = floor(xdiv(x, vs)), fy = floor(xdiv(y, vs)), fz = floor(xdiv(z, vs));
+            const double lim = double(KEY_LIM);
+            if (fx >= -lim && fx < lim && fy >= -lim && fy < lim && fz >= -lim && fz < lim) {
+                o = shard_of(pack_key(int64_t(fx), int64_t(fy), int64_t(fz)), world);
+                valid = true;
+            }
+        }
+        owner[i] = o;
+        atomicAdd(&h[o], 1u);
+        if (!valid) atomicAdd(&h[world], 1u);     // counted apart as well
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w <= world; w += blockDim.x)
+        if (h[w]) atomicAdd(counts + w, (unsigned long long)h[w]);
+}
+
+// rows of the owner-grouped permutation (stable: frame order within an owner)
+__global__ void k_gather_partition(const uint32_t* perm, int64_t n, int64_t gbase,
+                                   const double* __restrict__ xyz, const double* __restrict__ rgb,
+                                   double* oxyz, double* orgb, int64_t* ogidx) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int64_t i = perm[j];
+    oxyz[j * 3] = xyz[i * 3];
+    oxyz[j * 3 + 1] = xyz[i * 3 + 1];
+    oxyz[j * 3 + 2] = xyz[i * 3 + 2];
+    orgb[j * 3] = rgb[i * 3];
+    orgb[j * 3 + 1] = rgb[i * 3 + 1];
+    orgb[j * 3 + 2] = rgb[i * 3 + 2];
+    ogidx[j] = gbase + i;
+}
+
+int map_partition_by_owner(VxMap* m, const double* xyz, const double* rgb, int64_t n,
+                           int64_t gbase, double* oxyz, double* orgb, int64_t* ogidx,
+                           int64_t* h_counts, cudaStream_t s) {
+    const int world = m->cfg.shard_world > 1 ? m->cfg.shard_world : 1;
+    if (world > 64) {
+        set_error("input slicing supports up to 64 shards (got %d)", world);
+        return VX_E_INPUT;
+    }
+    for (int w = 0; w <= world; ++w) h_counts[w] = 0;
+    if (n <= 0) return VX_OK;
+    if (n >= (int64_t(1) << 31) - 1) {
+        set_error("slice of %lld points exceeds the 2^31 point limit", (long long)n);
+        return VX_E_INPUT;
+    }
+    VX_TRY(m->prank.reserve(n * 4, s));
+    VX_TRY(m->pidx.reserve(n * 4, s));
+    VX_TRY(m->prank2.reserve(n * 4, s));
+    VX_TRY(m->pidx2.reserve(n * 4, s));
+    VX_TRY(m->stage.reserve(65 * 8, s));
+    unsigned long long* dcnt = m->stage.as<unsigned long long>();
+    VX_CUDA(cudaMemsetAsync(dcnt, 0, 65 * 8, s));
+    k_owner_of_points<<<nblk(n), 256, 0, s>>>(xyz, n, m->cfg.voxel_size, world,
+                                              m->prank.as<uint32_t>(), dcnt);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    bool in_alt = false;
+    VX_TRY(radix_sort_pairs(m->prank.as<uint32_t>(), m->pidx.as<uint32_t>(), m->prank2.as<uint32_t>(),
+                            m->pidx2.as<uint32_t>(), n, bits_for(world - 1), m->sort_tmp, s, &in_alt,
+                            /*vals_identity=*/true));
+    const uint32_t* perm = in_alt ? m->pidx2.as<uint32_t>() : m->pidx.as<uint32_t>();
+    k_gather_partition<<<nblk(n), 256, 0, s>>>(perm, n, gbase, xyz, rgb, oxyz, orgb, ogidx);
+    count_launch();
+    VX_CHECK_LAUNCH();
+    unsigned long long hc[65];
+    VX_CUDA(cudaMemcpyAsync(hc, dcnt, size_t(world + 1) * 8, cudaMemcpyDeviceToHost, s));
+    VX_CUDA(cudaStreamSynchronize(s));
+    for (int w = 0; w <= world; ++w) h_counts[w] = int64_t(hc[w]);
+    return VX_OK;
+}
+
 // ------------------------------------------------------------------ store_frame
 static int map_store_frame_impl(VxMap* m, const double* xyz, const double* rgb, int64_t n,
                                 VxFrameInfo* info, cudaStream_t s);

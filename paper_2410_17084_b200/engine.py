@@ -110,8 +110,13 @@ class MappingEngine:
         keys = None
         if self.track_order:
             lf = N.view_tensor(v.last_first, (int(v.num_voxels),), np.int32)
-            keys = (int(frame_index) << 32) | lf.index_select(0, first.long()).long()
+            keys = (int(frame_index) << 32) | self._global_point(lf.index_select(0, first.long()).long())
         return first, keys
+
+    def _global_point(self, idx):
+        """Frame point numbers -> the scan's global row numbers (sliced ingest)."""
+        pi = getattr(self, "_point_index", None)
+        return idx if pi is None else pi.index_select(0, idx)
 
     def _append_orders(self, keys):
         import torch
@@ -153,7 +158,7 @@ class MappingEngine:
         nslot = int(slot.max().item()) + 1
         lf = N.view_tensor(v.last_first, (V,), np.int32).index_select(0, vids).long()
         return {"keys": N.view_tensor(v.keys, (V, 3), np.int64).index_select(0, vids),
-                "order": (int(v.frame_index) << 32) | lf,
+                "order": (int(v.frame_index) << 32) | self._global_point(lf),
                 "positions": N.view_tensor(v.pred_xyz, (nslot, M, 3), np.float64).index_select(0, slot),
                 "colors": N.view_tensor(v.pred_rgb, (nslot, M, 3), np.float64).index_select(0, slot),
                 "variances": N.view_tensor(v.pred_var, (nslot, M), np.float64).index_select(0, slot)}
@@ -330,8 +335,12 @@ class MappingEngine:
         return reports
 
     def ingest_device(self, d_xyz, d_rgb, n: int, camera=None, d_image=None,
-                      image_future=None) -> IngestReport:
+                      image_future=None, point_index=None) -> IngestReport:
+        """One frame of device-resident points.  `point_index` (int64, n): the
+        scan row number of each point when the frame is this rank's share of a
+        sliced scan (`ShardedEngine.ingest_sliced`); order keys then use it."""
         t0 = time.perf_counter()
+        self._point_index = point_index
         if d_image is not None and camera is not None:
             d_image = image_for_camera(camera, d_image)
         cfg = self.config

@@ -28,6 +28,7 @@ from __future__ import annotations
 import numpy as np
 
 from .engine import MappingEngine
+from .errors import InputDomainError
 
 KEY_BITS = 21
 KEY_BIAS = 1 << (KEY_BITS - 1)
@@ -174,6 +175,60 @@ class ShardedEngine:
     def ingest_device(self, d_xyz, d_rgb, n, camera=None, d_image=None):
         self._frame_first_record = self.engine.num_gaussians
         return self.engine.ingest_device(d_xyz, d_rgb, n, camera, d_image)
+
+    def ingest_sliced(self, d_xyz, d_rgb, n: int, global_base: int, camera=None, d_image=None):
+        """Ingest this rank's slice (rows [global_base, global_base + n)) of a
+        scan that is split over the ranks.
+
+        The slice's points are grouped by the rank owning their voxel
+        (`vx_map_partition_by_owner`), exchanged with one all-to-all (NCCL over
+        NVLink; under gloo through the host), and the points this rank receives
+        — its voxels' points of the whole scan, in global frame order since the
+        slices are contiguous and each group keeps frame order — are ingested
+        with their global row numbers as the order-key source.  Outputs equal
+        `ingest` of the whole scan on every rank (bit for bit after
+        `gather_frame`); each rank moves 1/world of the scan over PCIe.
+        """
+        import ctypes as C
+        import torch
+        import torch.distributed as dist
+        from . import _native as N
+        eng = self.engine
+        world = self.world
+        dev = N.device()
+        ox = torch.empty((max(n, 0), 3), dtype=torch.float64, device=dev)
+        oc = torch.empty_like(ox)
+        og = torch.empty(max(n, 0), dtype=torch.int64, device=dev)
+        counts = (C.c_int64 * (world + 1))()
+        vm = eng.vmap
+        h = vm._h()
+        N.check(vm._lib.vx_map_partition_by_owner(h, N.ptr(d_xyz), N.ptr(d_rgb), int(n),
+                                                   int(global_base), N.ptr(ox), N.ptr(oc),
+                                                   N.ptr(og), counts, N.stream_ptr()))
+        backend = dist.get_backend(self.group)
+        cdev = torch.device("cpu") if backend == "gloo" else dev
+        # rows without a voxel key fail the frame on EVERY rank (the reference
+        # rejects the frame; no rank may go on to the next collective alone)
+        bad = torch.tensor([int(counts[world])], dtype=torch.int64, device=cdev)
+        dist.all_reduce(bad, group=self.group)
+        if int(bad.item()):
+            raise InputDomainError(f"{int(bad.item())} scan points have no voxel key "
+                                   "(non-finite, or outside the lattice |k| < 2^20)")
+        send = torch.tensor(list(counts)[:world], dtype=torch.int64, device=cdev)
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=self.group)
+        ss, rs = [int(x) for x in send.tolist()], [int(x) for x in recv.tolist()]
+        tot = sum(rs)
+
+        def exchange(t, shape):
+            out = torch.empty((tot,) + shape, dtype=t.dtype, device=cdev)
+            dist.all_to_all_single(out, _staged(t, backend), output_split_sizes=rs,
+                                   input_split_sizes=ss, group=self.group)
+            return out.to(dev) if out.device != dev else out
+
+        rx, rc, rg = exchange(ox, (3,)), exchange(oc, (3,)), exchange(og, ())
+        self._frame_first_record = eng.num_gaussians
+        return eng.ingest_device(rx, rc, tot, camera, d_image, point_index=rg)
 
     def reset(self):
         self.engine.reset()

@@ -53,7 +53,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank_main(rank, world, port, threshold, outdir):
+def _rank_main(rank, world, port, threshold, outdir, sliced=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -63,7 +63,15 @@ def _rank_main(rank, world, port, threshold, outdir):
         from paper_2410_17084_b200 import sharding
         eng = sharding.ShardedEngine(_config(threshold), rank, world)
         for f, (pos, col, pin, img) in enumerate(_frames()):
-            eng.ingest(pos, col, _camera(pin), img)
+            if sliced:
+                # input slicing: this rank H2Ds rows [lo, hi) of the scan only
+                lo, hi = rank * len(pos) // world, (rank + 1) * len(pos) // world
+                dx = torch.from_numpy(np.ascontiguousarray(pos[lo:hi])).cuda()
+                dc = torch.from_numpy(np.ascontiguousarray(col[lo:hi])).cuda()
+                di = torch.from_numpy(img).cuda()
+                eng.ingest_sliced(dx, dc, hi - lo, lo, _camera(pin), di)
+            else:
+                eng.ingest(pos, col, _camera(pin), img)
             out = eng.gather_frame(dst=0)
             if rank == 0:
                 np.savez(os.path.join(outdir, f"frame{f}.npz"),
@@ -76,8 +84,11 @@ def _rank_main(rank, world, port, threshold, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("threshold", [1, 2500])
-def test_two_shards_equal_unsharded(threshold):
+@pytest.mark.parametrize("threshold,sliced", [(1, False), (2500, False), (1, True), (2500, True)])
+def test_two_shards_equal_unsharded(threshold, sliced):
+    """sliced: each rank holds half of every scan and the points reach their
+    owners through `ingest_sliced`'s all-to-all (order keys from the global
+    row numbers); the outputs must still equal the unsharded run."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_2410_17084_b200 as vx
@@ -99,7 +110,8 @@ def test_two_shards_equal_unsharded(threshold):
     with tempfile.TemporaryDirectory() as d:
         ctx = mp.get_context("spawn")
         port = _free_port()
-        procs = [ctx.Process(target=_rank_main, args=(r, 2, port, threshold, d)) for r in range(2)]
+        procs = [ctx.Process(target=_rank_main, args=(r, 2, port, threshold, d, sliced))
+                 for r in range(2)]
         for p in procs:
             p.start()
         for p in procs:
