@@ -194,7 +194,7 @@ class MappingEngine:
         return rep
 
     def ingest_stream(self, frames, reset_each: bool = False, on_frame=None,
-                      fetch_records: bool = False, on_records=None) -> list:
+                      fetch_records: bool = False, on_records=None, ingest_fn=None) -> list:
         """Ingest a sequence of host frames with H2D double-buffering.
 
         `frames` yields (positions, colors, camera, image) with positions /
@@ -210,6 +210,8 @@ class MappingEngine:
         stream, overlapped with the next frame's device work;
         `on_records(report, host_fields)` receives them once they have landed
         (the dict's tensors are reused two frames later: copy what you keep).
+        `ingest_fn(d_xyz, d_rgb, n, camera, d_image)` replaces `ingest_device`
+        for each frame (e.g. `ShardedEngine.ingest_sliced` of this rank's slice).
         """
         import torch
         dev = N.device()
@@ -318,7 +320,7 @@ class MappingEngine:
                     if self._drec_free[k & 1] is not None:
                         compute.wait_event(self._drec_free[k & 1])
             first = self.num_gaussians
-            rep = self.ingest_device(dx, dc, n, cam, di)
+            rep = (ingest_fn or self.ingest_device)(dx, dc, n, cam, di)
             if reset_each and fetch_records:
                 self._drec[k & 1] = self.records
             reports.append(rep)
