@@ -2742,7 +2742,7 @@ __global__ void __launch_bounds__(1024) k_sort_items_desc(VoxelSolveArgs va, Pro
 static int panel_team_size(int num_items) {
     if (const char* e = getenv("VX_PANEL_C")) {
         const int c = atoi(e);
-        if (c == 1 || c == 2 || c == 4 || c == 8) return c;
+        if (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) return c;
     }
     // up to two rounds of the team count: the largest voxel (first in the
     // queue) sets the latency, so bigger teams win (config 3: ~30 items)
@@ -2768,6 +2768,7 @@ static int launch_panel(const VoxelSolveArgs& va_in, const ProblemArgs& pa_in, i
     const size_t smem = size_t(lay.total) * sizeof(double);
     auto kfn = gpr_panel_kernel<VOXEL>;
     VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (C > 8) VX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int per_sm = 1;
     VX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, PNT, smem));
     if (per_sm < 1) per_sm = 1;

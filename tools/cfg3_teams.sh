@@ -18,4 +18,4 @@ for i in range(10):
 c = np.bincount(np.unique(np.floor(pos / 0.5).astype(np.int64), axis=0, return_counts=True)[1] > 160)
 print(f"wall {np.median(walls[3:])*1e3:.3f} ms, n_large {p['gpr_n_large'][0]:.3f} ms, voxels n>160: {c}")
 PY
-for C in auto 2 4 8; do if [ $C = auto ]; then unset VX_PANEL_C; else export VX_PANEL_C=$C; fi; echo "C=$C"; timeout 120 python /tmp/cfg3.py; done
+for C in auto 8 16; do if [ $C = auto ]; then unset VX_PANEL_C; else export VX_PANEL_C=$C; fi; echo "C=$C"; timeout 120 python /tmp/cfg3.py; done
