@@ -220,3 +220,38 @@ def test_stream_frames_ingest_equals_host_ingest():
     ga, gb = a.gaussians_device(), b.gaussians_device()
     for k in gb:
         assert ga[k].shape == gb[k].shape and bool((ga[k] == gb[k]).all()), k
+
+
+def test_partition_by_owner_groups_in_frame_order():
+    """vx_map_partition_by_owner (input slicing): rows grouped by the owner of
+    their voxel (sharding.owner_of, the host restatement of the device owner
+    test), frame order inside each group, global row numbers carried, rows
+    without a key counted apart and sent to rank 0."""
+    import ctypes as C
+    import torch
+    from paper_2410_17084_b200 import _native as N
+    from paper_2410_17084_b200 import sharding
+    from paper_2410_17084_b200.voxel_map import VoxelMap
+    rng = np.random.default_rng(3)
+    world, n, base = 3, 5000, 123456
+    pos = rng.uniform(-20, 20, (n, 3))
+    pos[17] = np.nan                                   # no key -> rank 0, counted apart
+    col = rng.uniform(0, 1, (n, 3))
+    vm = VoxelMap(0.5, 1e-4, 10, 0.3, shard_rank=1, shard_world=world)
+    h = vm._h()
+    dx, dc = torch.from_numpy(pos).cuda(), torch.from_numpy(col).cuda()
+    ox, oc = torch.empty_like(dx), torch.empty_like(dc)
+    og = torch.empty(n, dtype=torch.int64, device="cuda")
+    counts = (C.c_int64 * (world + 1))()
+    N.check(vm._lib.vx_map_partition_by_owner(h, N.ptr(dx), N.ptr(dc), n, base, N.ptr(ox),
+                                               N.ptr(oc), N.ptr(og), counts, N.stream_ptr()))
+    ok = np.isfinite(pos).all(axis=1)
+    keys = np.floor(pos[ok] / 0.5).astype(np.int64)
+    own = np.zeros(n, dtype=np.int64)
+    own[ok] = sharding.owner_of(keys, world)
+    want = np.concatenate([np.nonzero(own == w)[0] for w in range(world)])
+    assert list(counts)[:world] == [int((own == w).sum()) for w in range(world)]
+    assert counts[world] == 1
+    np.testing.assert_array_equal(og.cpu().numpy(), base + want)
+    np.testing.assert_array_equal(ox.cpu().numpy(), pos[want])
+    np.testing.assert_array_equal(oc.cpu().numpy(), col[want])
