@@ -156,3 +156,28 @@ def test_image_for_camera_crops_and_rejects():
         except IndexError:
             continue
         raise AssertionError(f"shape {bad.shape} accepted")
+
+
+def test_event_log_materialises_transitions_on_read():
+    """transitions / solve_log are numpy-backed read-only lists: same rows,
+    order and types as the per-event objects they replace (a first solve that
+    converges passes through ACTIVE, voxel_map.py:250-261)."""
+    import numpy as np
+    from paper_2410_17084_b200.voxel_map import StateTransition, VoxelKey, VoxelMap, VoxelState
+    vm = VoxelMap(0.5, 1e-4, 10, 0.3)
+    k = np.array([[1, 2, 3], [4, 5, 6], [7, 8, 9]], dtype=np.int64)
+    vm._events.append(("t", 0, k, np.array([0, 0, 0]), np.array([1, 1, 1])))
+    # solves: READY->ACTIVE, READY->CONVERGED (two steps), ACTIVE->ACTIVE (re-fit, none)
+    vm._events.append(("s", 1, k, np.array([1, 1, 2]), np.array([2, 3, 2])))
+    tr = vm.transitions
+    want = [StateTransition(0, VoxelKey(1, 2, 3), VoxelState.UNREADY, VoxelState.READY),
+            StateTransition(0, VoxelKey(4, 5, 6), VoxelState.UNREADY, VoxelState.READY),
+            StateTransition(0, VoxelKey(7, 8, 9), VoxelState.UNREADY, VoxelState.READY),
+            StateTransition(1, VoxelKey(1, 2, 3), VoxelState.READY, VoxelState.ACTIVE),
+            StateTransition(1, VoxelKey(4, 5, 6), VoxelState.READY, VoxelState.ACTIVE),
+            StateTransition(1, VoxelKey(4, 5, 6), VoxelState.ACTIVE, VoxelState.CONVERGED)]
+    assert len(tr) == 6 and list(tr) == want and tr == want
+    assert tr[-1] == want[-1] and tr[3:5] == want[3:5]
+    assert type(tr[0].key) is VoxelKey and tr[0].new is VoxelState.READY
+    assert list(vm.solve_log) == [(1, VoxelKey(*r)) for r in k.tolist()]
+    assert vm.audit_transitions() == []
